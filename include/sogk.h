@@ -1,0 +1,233 @@
+/*
+ * sogk.h — C-ABI of the B200-native ray sampler (arXiv 2404.10272 hot path).
+ *
+ * The reference (`/root/reference/proj/include/sog/`, namespace `sog`) is a
+ * header-only C++20 CPU library with no FFI; its drop-in boundary is its own
+ * C++ entry points for grid build, traverse and sample.  This header is the
+ * flat C surface those entry points map onto (plain pointers and sizes, no
+ * C++ or torch types); `sogk_sog.hpp` is the C++ shim that keeps the
+ * reference signatures on top of it.  Each entry point cites the reference
+ * interface it replaces.
+ *
+ * Conventions
+ *  - Every function returns an int status (sogk_status); no exceptions cross
+ *    the boundary.  sogk_last_error() returns the thread-local message of the
+ *    last failure.
+ *  - Device buffers ("d_" prefix) are caller-owned CUDA device pointers;
+ *    host buffers ("h_" prefix) are caller-owned host pointers (pinned memory
+ *    recommended).  `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Grids are immutable after creation and may be shared by samplers, host
+ *    threads and streams (mirrors the reference, README "Concurrency").
+ *    A sampler owns scratch memory: use one sampler per concurrent stream.
+ *  - Rays are the reference `sog::Ray` layout (ray.hpp:92-114): 8 doubles per
+ *    ray {origin.xyz, direction.xyz, t_min, t_max}, i.e. a std::vector<sog::Ray>
+ *    can be passed as is.
+ *
+ * Output contract (the reference returns a per-ray
+ * std::vector<double>, sampling.hpp:42,157-164):
+ *    packed_info[r] = {offset_r, count_r}   (int64 pairs, exclusive scan of counts in ray order)
+ *    t_starts[offset_r + k] = S_r[k]        (the reference sample buffer, bit-exact)
+ *    t_ends  [offset_r + k] = S_r[k] + step(S_r[k])   (the next t_last, sampling.hpp:99,118)
+ *    ray_indices[offset_r + k] = ray_index_base + r
+ *    cells[...]  = ijk of the emitting event packed x | y<<10 | z<<20
+ *                  (voxel for DDA, node origin for HDDA)
+ *    levels[...] = event Level (grid.hpp:75) | cascade grid_level << 2
+ */
+#ifndef SOGK_H
+#define SOGK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SOGK_ABI_VERSION 1
+#define SOGK_MAX_LEVELS 8
+#define SOGK_DEFAULT_SPIN_CAP 64
+
+typedef enum {
+    SOGK_OK = 0,
+    SOGK_INVALID_ARG = 1,           /* std::invalid_argument / std::out_of_range in the reference */
+    SOGK_CUDA_ERROR = 2,
+    SOGK_OOM = 3,
+    SOGK_INSUFFICIENT_CAPACITY = 4, /* host/device output buffers too small (stats hold the total) */
+    SOGK_IO_ERROR = 5,              /* sog::io_error (io.hpp:17-36); message carries the io_errc */
+    SOGK_NO_DEVICE = 6
+} sogk_status;
+
+/* per-ray status (uint8) */
+enum {
+    SOGK_RAY_OK = 0,
+    SOGK_RAY_INVALID = 1,   /* would throw in sog::Ray's constructor (ray.hpp:98-106) */
+    SOGK_RAY_UNDEFINED = 2  /* reference HddaTraversal::next never returns (traversal.hpp:238-241) */
+};
+
+typedef enum { SOGK_DDA = 0, SOGK_HDDA = 1 } sogk_analyzer;       /* bench.hpp:27 AnalyzerKind */
+typedef enum { SOGK_BRANCH = 0, SOGK_SKIP = 1 } sogk_kernel;       /* sampling.hpp:155 KernelKind */
+typedef enum { SOGK_CONSTANT = 0, SOGK_LINEAR = 1 } sogk_schedule; /* sampling.hpp:18-39 */
+typedef enum { SOGK_GRID_DENSE = 0, SOGK_GRID_VDB = 1 } sogk_grid_kind;
+typedef enum { SOGK_BLOBS = 0, SOGK_SHELL = 1, SOGK_SPONGE = 2, SOGK_RANDOM = 3 } sogk_scene_kind;
+
+/* stats block written by sogk_sample_count (int64[SOGK_STATS_LEN], device) */
+enum {
+    SOGK_STAT_TOTAL_SAMPLES = 0,
+    SOGK_STAT_INVALID_RAYS = 1,
+    SOGK_STAT_UNDEFINED_RAYS = 2,
+    SOGK_STAT_ANALYZER_LOOKUPS = 3, /* sum of SampleRun::analyzer_lookups */
+    SOGK_STAT_ANALYZER_STEPS = 4,   /* sum of SampleRun::analyzer_steps */
+    SOGK_STAT_KERNEL_LOOKUPS = 5,   /* sum of SampleRun::kernel_lookups */
+    SOGK_STATS_LEN = 8
+};
+
+typedef struct sogk_grid sogk_grid;
+typedef struct sogk_sampler sogk_sampler;
+
+/* sog::GridTransform (grid.hpp:18-70) */
+typedef struct {
+    int32_t res[3];
+    double world_min[3];
+    double voxel_size;
+} sogk_transform;
+
+typedef struct {
+    int32_t kind;           /* sogk_grid_kind */
+    sogk_transform transform;
+    int64_t root_entries;   /* SparseGrid::root().size() (VDB) */
+    int64_t internal_nodes; /* root entries of kind internal */
+    int64_t leaf_count;     /* SparseGrid::leaf_count() (sparse.hpp:173-178) */
+    int64_t memory_bytes;   /* sog::memory_bytes (io.hpp:223-238) */
+    int64_t device_bytes;   /* HBM footprint of this handle */
+} sogk_grid_info;
+
+typedef struct {
+    int32_t analyzer;  /* sogk_analyzer; DDA needs dense levels, HDDA needs VDB levels */
+    int32_t kernel;    /* sogk_kernel */
+    int32_t schedule;  /* sogk_schedule */
+    double dt0;        /* StepSchedule::constant(dt) / linear(dt0, growth) */
+    double growth;
+    int32_t cascade;   /* 1: run_cascade_sampler (sampling.hpp:440-455) even for one level;
+                          n_levels > 1 always means a cascade */
+    int32_t spin_cap;  /* consecutive degenerate HDDA iterations before SOGK_RAY_UNDEFINED; 0 = 64 */
+} sogk_sampler_desc;
+
+/* Pinhole camera with the host-side part of Camera::pixel_ray precomputed
+ * (camera.hpp:167-173: forward/right/cam_up/tan_half/aspect; std::tan stays on the host). */
+typedef struct {
+    double position[3];
+    double forward[3];
+    double right[3];
+    double cam_up[3];
+    double tan_half;
+    double aspect;
+    double t_far;
+    int32_t width, height;
+} sogk_camera;
+
+/* ---- library ----------------------------------------------------------- */
+const char* sogk_version(void);
+int sogk_abi_version(void);
+const char* sogk_status_string(int status);
+/* copies the calling thread's last error message into buf; returns its full length */
+int sogk_last_error(char* buf, size_t len);
+/* number of visible CUDA devices (0 on a CPU-only host) */
+int sogk_device_count(void);
+
+/* ---- grids ------------------------------------------------------------- */
+/* DenseGrid(transform) + payload (grid.hpp:120-124): host bit payload, ceil(N/8) bytes */
+int sogk_grid_create_dense(const sogk_transform* t, const uint8_t* h_bits, size_t nbytes,
+                           void* stream, sogk_grid** out);
+/* same from a device payload (e.g. after an NCCL broadcast); the bytes are copied */
+int sogk_grid_create_dense_device(const sogk_transform* t, const uint8_t* d_bits, size_t nbytes,
+                                  void* stream, sogk_grid** out);
+/* build_sparse (sparse.hpp:333-371) on the GPU: ballot/popc masks + prefix-scan leaf slots */
+int sogk_grid_build_vdb(const sogk_grid* dense, void* stream, sogk_grid** out);
+/* deserialize_dense / deserialize_sparse (io.hpp:143-151, 183-214) straight to HBM */
+int sogk_grid_load_sog0(const uint8_t* bytes, size_t len, void* stream, sogk_grid** out);
+int sogk_grid_load_sog1(const uint8_t* bytes, size_t len, void* stream, sogk_grid** out);
+/* serialize_dense / serialize_sparse (io.hpp:134-141, 161-181).  buf == NULL queries *len. */
+int sogk_grid_export_sog0(const sogk_grid* dense, uint8_t* buf, size_t* len);
+int sogk_grid_export_sog1(const sogk_grid* vdb, uint8_t* buf, size_t* len);
+/* DenseGrid::payload() back to the host (to_dense for a VDB, sparse.hpp:374-383) */
+int sogk_grid_download_dense(const sogk_grid* g, uint8_t* h_bits, size_t nbytes);
+int sogk_grid_get_info(const sogk_grid* g, sogk_grid_info* out);
+int sogk_grid_destroy(sogk_grid* g);
+
+/* ---- samplers ---------------------------------------------------------- */
+/* make_sampler (bench.hpp:382-413) for one variant: validates the schedule
+ * (StepSchedule, sampling.hpp:25-34) and the cascade (validate_cascade, :253-273). */
+int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
+                        const sogk_sampler_desc* desc, sogk_sampler** out);
+int sogk_sampler_destroy(sogk_sampler* s);
+
+/* Pass 1 of run_sampler / run_cascade_sampler over a batch (sampling.hpp:166-196, 440-455):
+ * per-ray sample counts, exclusive-scanned on the device into d_packed_info[n][2]
+ * (single-pass decoupled look-back).  d_stats (int64[SOGK_STATS_LEN]) is overwritten.
+ * d_status (uint8[n]) and d_counters (int32[n][3] = analyzer_lookups, analyzer_steps,
+ * kernel_lookups) are optional (NULL). */
+int sogk_sample_count(sogk_sampler* s, const double* d_rays, int64_t n, int64_t* d_packed_info,
+                      int64_t* d_stats, uint8_t* d_status, int32_t* d_counters, void* stream);
+/* Pass 2: writes the packed samples at the offsets of d_packed_info.  Buffers must hold
+ * stats[SOGK_STAT_TOTAL_SAMPLES] entries; d_cells / d_levels / d_t_ends / d_ray_indices
+ * may be NULL. */
+int sogk_sample_write(sogk_sampler* s, const double* d_rays, int64_t n,
+                      const int64_t* d_packed_info, int64_t ray_index_base, double* d_t_starts,
+                      double* d_t_ends, int32_t* d_ray_indices, uint32_t* d_cells,
+                      uint8_t* d_levels, void* stream);
+/* Camera-fused variants: the rays of pixels [first_pixel, first_pixel + n) are generated
+ * in registers (Camera::pixel_ray, camera.hpp:167-179) instead of read from HBM. */
+int sogk_sample_count_camera(sogk_sampler* s, const sogk_camera* cam, int64_t first_pixel,
+                             int64_t n, int64_t* d_packed_info, int64_t* d_stats,
+                             uint8_t* d_status, int32_t* d_counters, void* stream);
+int sogk_sample_write_camera(sogk_sampler* s, const sogk_camera* cam, int64_t first_pixel,
+                             int64_t n, const int64_t* d_packed_info, int64_t ray_index_base,
+                             double* d_t_starts, double* d_t_ends, int32_t* d_ray_indices,
+                             uint32_t* d_cells, uint8_t* d_levels, void* stream);
+
+/* End-to-end from HOST buffers: H2D rays, count, scan, write, D2H of every output
+ * (the batched form of calling run_sampler per ray).  When the total exceeds
+ * `capacity` the call returns SOGK_INSUFFICIENT_CAPACITY with h_stats filled and
+ * h_packed_info valid; outputs may be NULL to skip them. */
+int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t ray_index_base,
+                     int64_t capacity, int64_t* h_packed_info, double* h_t_starts,
+                     double* h_t_ends, int32_t* h_ray_indices, uint32_t* h_cells,
+                     uint8_t* h_levels, uint8_t* h_status, int32_t* h_counters,
+                     int64_t* h_stats, void* stream);
+
+/* ---- rays -------------------------------------------------------------- */
+/* host: Camera::pixel_ray's per-camera terms (camera.hpp:158-173) */
+int sogk_camera_setup(const double position[3], const double target[3], const double up[3],
+                      double vfov_deg, int32_t width, int32_t height, double t_far,
+                      sogk_camera* out);
+/* device: rays of pixels [first_pixel, first_pixel + n), row-major (px fastest) */
+int sogk_camera_rays(const sogk_camera* cam, int64_t first_pixel, int64_t n, double* d_rays,
+                     void* stream);
+/* host twin of sogk_camera_rays (bit-identical) */
+int sogk_camera_rays_host(const sogk_camera* cam, int64_t first_pixel, int64_t n,
+                          double* h_rays);
+
+/* ---- host input generators (deterministic; no GPU needed) ---------------
+ * Restatements of the reference generators so that identical inputs can be
+ * produced where the reference is absent (tests pin them to the reference). */
+/* generate_scene (scene_gen.hpp:94-192); *occupancy = occupancy_fraction() */
+int sogk_scene_generate(int kind, const sogk_transform* t, uint64_t seed, double fraction,
+                        int32_t count, double threshold, uint8_t* h_bits, double* occupancy);
+/* build_dense_cascade (scene_gen.hpp:196-209) of generate_scene(kind, base, ...):
+ * levels consecutive payloads; out_transforms[levels] */
+int sogk_scene_cascade(int kind, const sogk_transform* base, uint64_t seed, double fraction,
+                       int32_t count, double threshold, int32_t levels, uint8_t* h_bits,
+                       sogk_transform* out_transforms);
+/* make_probe_rays (bench.hpp:628-649) */
+int sogk_probe_rays(const sogk_transform* t, int64_t count, uint64_t seed, double* h_rays);
+/* testsupport::random_ray x count from one mt19937_64(seed) (tests/support/test_support.hpp:66-82) */
+int sogk_random_rays(const sogk_transform* t, int64_t count, uint64_t seed, double* h_rays);
+/* testsupport::random_grid / random_blocky_grid (test_support.hpp:29-62) */
+int sogk_random_grid(const sogk_transform* t, uint64_t seed, double fraction, uint8_t* h_bits);
+int sogk_random_blocky_grid(const sogk_transform* t, uint64_t seed, double block_fraction,
+                            double noise_fraction, uint8_t* h_bits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOGK_H */

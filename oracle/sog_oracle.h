@@ -1,0 +1,95 @@
+/*
+ * sog_oracle.h — CPU restatement of the reference ray-sampler path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing under oracle/ is part of the product:
+ * only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load it, and only as the checker.
+ *
+ * This is a plain-C restatement of the reference's header-only C++ library
+ * (`/root/reference/proj/include/sog/*.hpp`); every function cites the
+ * reference file:line it follows.  It is compiled FMA-free
+ * (-ffp-contract=off, no -march) exactly like the reference CMake build, so
+ * its FP64 results are bit-identical to the reference's.
+ *
+ * Parity pinning: tests/test_oracle.py checks this restatement against
+ *  (1) the known-answer tests of the reference's own unit suite
+ *      (proj/tests/unit/test_sampling.cpp, test_traversal.cpp,
+ *       test_vdb_tree.cpp) re-expressed in Python, and
+ *  (2) golden vectors produced by the unmodified reference headers
+ *      (oracle/ref_shim.cpp -> oracle/_ref/libsogref.so, fixtures committed
+ *      under tests/golden/ by tests/golden/make_golden.py).
+ */
+#ifndef SOG_ORACLE_H
+#define SOG_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct og_grid og_grid;
+
+/* analyzer / kernel / schedule / status codes (same values as include/sogk.h) */
+enum { OG_DDA = 0, OG_HDDA = 1 };
+enum { OG_BRANCH = 0, OG_SKIP = 1 };
+enum { OG_CONSTANT = 0, OG_LINEAR = 1 };
+enum { OG_RAY_OK = 0, OG_RAY_INVALID = 1, OG_RAY_UNDEFINED = 2 };
+
+typedef struct {
+    int32_t ijk[3];
+    int32_t level;      /* sog::Level: 0 leaf_voxel, 1 leaf_tile, 2 internal_tile, 3 root_tile */
+    double t0, t1;
+    int32_t occupied;
+    int32_t grid_level; /* cascade level, -1 outside every level; 0 for single grids */
+} og_event;
+
+typedef struct {
+    const og_grid* levels[8];
+    int32_t n_levels;
+    int32_t cascade;    /* 1: CascadeTraversal (sampling.hpp:305-415) even for one level */
+    int32_t analyzer;   /* OG_DDA (dense levels) / OG_HDDA (sparse levels) */
+    int32_t kernel;     /* OG_BRANCH / OG_SKIP */
+    int32_t sched_kind; /* OG_CONSTANT / OG_LINEAR */
+    double dt0, growth;
+    int32_t spin_cap;   /* consecutive degenerate HDDA iterations before REF_UNDEFINED */
+} og_sampler;
+
+/* grids ------------------------------------------------------------------ */
+og_grid* og_dense_create(const int32_t res[3], const double wmin[3], double voxel,
+                         const uint8_t* bits);
+og_grid* og_sparse_build(const og_grid* dense);            /* sparse.hpp:333-371 */
+void og_grid_free(og_grid* g);
+int64_t og_sparse_serialize(const og_grid* sparse, uint8_t* buf, int64_t cap); /* io.hpp:161-181 */
+int64_t og_sparse_leaf_count(const og_grid* sparse);
+int32_t og_dense_voxel_at(const og_grid* dense, const int32_t ijk[3]);          /* grid.hpp:129-133 */
+/* query -> occupied; writes level, origin[3], extent (sparse.hpp:163-214) */
+int32_t og_sparse_query(const og_grid* sparse, const int32_t ijk[3], int32_t* level,
+                        int32_t origin[3], int32_t* extent);
+
+/* traversal ---------------------------------------------------------------- */
+/* Drains the sampler's analyzer for one ray into `events` (up to cap); returns the
+ * event count, or -1 when the HDDA spin guard fired.  counters = {lookups, steps}. */
+int64_t og_collect_events(const og_sampler* s, const double ray[8], int64_t cap,
+                          og_event* events, int64_t counters[2]);
+
+/* sampling ----------------------------------------------------------------- */
+/* One ray through run_sampler / run_cascade_sampler (sampling.hpp:166-196,440-455).
+ * Returns the sample count (may exceed cap; only cap samples are written).
+ * counters = {analyzer_lookups, analyzer_steps, kernel_lookups}. */
+int64_t og_sample_ray(const og_sampler* s, const double ray[8], int64_t cap, double* t_starts,
+                      double* t_ends, uint32_t* cells, uint8_t* levels, int64_t counters[3],
+                      int32_t* status);
+
+/* Batched packed output, same contract as sogk_sample_count + sogk_sample_write.
+ * Returns the total sample count; when total > cap nothing past cap is written
+ * (call again with a larger cap).  Any output pointer may be NULL. */
+int64_t og_sample_batch(const og_sampler* s, const double* rays, int64_t n,
+                        int64_t ray_index_base, int64_t cap, int64_t* packed_info,
+                        double* t_starts, double* t_ends, int32_t* ray_indices, uint32_t* cells,
+                        uint8_t* levels, int32_t* counters, uint8_t* status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

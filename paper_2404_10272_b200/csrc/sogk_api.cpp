@@ -1,0 +1,936 @@
+// sogk_api.cpp — the C-ABI (include/sogk.h): grid and sampler handles, SOG0/SOG1
+// I/O, validation with the reference's error semantics, and the launchers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "sogk.h"
+#include "sogk_internal.h"
+
+using namespace sogk;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+
+int fail(int status, const std::string& msg) {
+    g_err = msg;
+    return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        return fail(SOGK_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+        return fail(SOGK_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+    return fail(SOGK_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                   \
+    do {                                                 \
+        cudaError_t _e = (expr);                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+bool valid_transform(const sogk_transform* t) { // GridTransform ctor, grid.hpp:24-30
+    return t && t->res[0] >= 1 && t->res[1] >= 1 && t->res[2] >= 1 && t->voxel_size > 0.0;
+}
+uint64_t voxel_count(const sogk_transform& t) { return uint64_t(t.res[0]) * t.res[1] * t.res[2]; }
+uint64_t payload_bytes(const sogk_transform& t) { return (voxel_count(t) + 7) / 8; }
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+struct RootEntry { // one record of the reference root map (sparse.hpp:143-150)
+    int32_t origin[3];
+    uint8_t kind; // 0 empty tile, 1 occupied tile, 2 internal
+    int32_t node; // region slot for internal entries
+};
+
+struct RegionOrder { // sparse.hpp:119-125
+    bool operator()(const std::array<int32_t, 3>& a, const std::array<int32_t, 3>& b) const {
+        if (a[2] != b[2]) return a[2] < b[2];
+        if (a[1] != b[1]) return a[1] < b[1];
+        return a[0] < b[0];
+    }
+};
+} // namespace
+
+struct sogk_grid {
+    int kind = SOGK_GRID_DENSE;
+    sogk_transform t{};
+    int device = 0;
+    // dense
+    uint8_t* bits = nullptr;
+    uint64_t nbytes = 0;
+    // vdb
+    int R[3] = {0, 0, 0};
+    int64_t nreg = 0;
+    int32_t* root = nullptr;
+    uint64_t* child_mask = nullptr;
+    uint64_t* value_mask = nullptr;
+    uint32_t* prefix = nullptr;
+    uint64_t* leaves = nullptr;
+    uint32_t* region_leaves = nullptr;
+    uint32_t* total_leaves = nullptr;
+    uint64_t leaf_capacity = 0;
+    // host-side root map when loaded from SOG1 (entries that do not map to an
+    // in-grid aligned region are kept for export only); empty for built grids
+    std::vector<RootEntry> extra_entries;
+    bool from_file = false;
+    // lazily materialized metadata
+    mutable bool meta_ready = false;
+    mutable std::vector<int32_t> h_root;
+    mutable int64_t leaf_count = 0;
+
+    ~sogk_grid() {
+        cudaFree(bits);
+        cudaFree(root);
+        cudaFree(child_mask);
+        cudaFree(value_mask);
+        cudaFree(prefix);
+        cudaFree(leaves);
+        cudaFree(region_leaves);
+        cudaFree(total_leaves);
+    }
+
+    GridDev dev() const {
+        GridDev g{};
+        for (int a = 0; a < 3; ++a) {
+            g.res[a] = t.res[a];
+            g.wmin[a] = t.world_min[a];
+            g.R[a] = R[a];
+        }
+        g.voxel = t.voxel_size;
+        const double h = t.voxel_size * 0.5; // center_bounds, sampling.hpp:248-251
+        for (int a = 0; a < 3; ++a) {
+            g.clo[a] = t.world_min[a] + h;
+            g.chi[a] = (t.world_min[a] + double(t.res[a]) * t.voxel_size) - h;
+        }
+        g.bits = bits;
+        g.root = root;
+        g.child_mask = child_mask;
+        g.value_mask = value_mask;
+        g.prefix = prefix;
+        g.leaves = leaves;
+        return g;
+    }
+
+    int fetch_meta() const {
+        if (meta_ready) return SOGK_OK;
+        if (kind != SOGK_GRID_VDB) {
+            meta_ready = true;
+            return SOGK_OK;
+        }
+        h_root.resize(nreg);
+        CK(cudaMemcpy(h_root.data(), root, nreg * sizeof(int32_t), cudaMemcpyDeviceToHost), "root D2H");
+        uint32_t tl = 0;
+        CK(cudaMemcpy(&tl, total_leaves, sizeof(uint32_t), cudaMemcpyDeviceToHost), "leaf count D2H");
+        leaf_count = tl;
+        meta_ready = true;
+        return SOGK_OK;
+    }
+};
+
+struct sogk_sampler {
+    Variant v{};
+    SamplerDev dev{};
+    sogk_sampler_desc desc{};
+    int n_levels = 0;
+    // count-pass scratch: tile states + dynamic tile counter
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    // sogk_sample_host scratch
+    void* hb = nullptr;
+    size_t hb_bytes = 0;
+
+    ~sogk_sampler() {
+        cudaFree(ws);
+        cudaFree(hb);
+    }
+
+    int ensure_ws(int64_t n) {
+        const int64_t blocks = (n + 255) / 256;
+        const size_t need = size_t(blocks) * 8 + 16;
+        if (need <= ws_bytes) return SOGK_OK;
+        cudaFree(ws);
+        ws = nullptr;
+        ws_bytes = 0;
+        CK(cudaMalloc(&ws, need), "sampler workspace");
+        ws_bytes = need;
+        return SOGK_OK;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// library
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* sogk_version(void) { return "sogk 0.1.0 (sm_100a)"; }
+int sogk_abi_version(void) { return SOGK_ABI_VERSION; }
+
+const char* sogk_status_string(int s) {
+    switch (s) {
+        case SOGK_OK: return "ok";
+        case SOGK_INVALID_ARG: return "invalid argument";
+        case SOGK_CUDA_ERROR: return "CUDA error";
+        case SOGK_OOM: return "out of device memory";
+        case SOGK_INSUFFICIENT_CAPACITY: return "insufficient output capacity";
+        case SOGK_IO_ERROR: return "I/O error";
+        case SOGK_NO_DEVICE: return "no CUDA device";
+        default: return "unknown status";
+    }
+}
+
+int sogk_last_error(char* buf, size_t len) {
+    if (buf && len) {
+        const size_t n = std::min(len - 1, g_err.size());
+        std::memcpy(buf, g_err.data(), n);
+        buf[n] = 0;
+    }
+    return int(g_err.size());
+}
+
+int sogk_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// grids
+// ---------------------------------------------------------------------------
+static int create_dense(const sogk_transform* t, const uint8_t* bits, size_t nbytes, bool host,
+                        void* stream, sogk_grid** out) {
+    if (!out) return fail(SOGK_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!valid_transform(t))
+        return fail(SOGK_INVALID_ARG, "grid resolution components must be >= 1 and voxel size positive");
+    if (!bits) return fail(SOGK_INVALID_ARG, "bit payload is NULL");
+    if (nbytes != payload_bytes(*t))
+        return fail(SOGK_INVALID_ARG, "payload size must be ceil(voxel_count / 8) bytes");
+    auto* g = new sogk_grid;
+    g->kind = SOGK_GRID_DENSE;
+    g->t = *t;
+    g->nbytes = nbytes;
+    cudaGetDevice(&g->device);
+    cudaError_t e = dalloc(&g->bits, nbytes);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(g->bits, bits, nbytes,
+                            host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, S(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream)); // caller may free its buffer
+    if (e != cudaSuccess) {
+        delete g;
+        return cuda_fail(e, "dense grid upload");
+    }
+    *out = g;
+    return SOGK_OK;
+}
+
+int sogk_grid_create_dense(const sogk_transform* t, const uint8_t* h_bits, size_t nbytes,
+                           void* stream, sogk_grid** out) {
+    return create_dense(t, h_bits, nbytes, true, stream, out);
+}
+
+int sogk_grid_create_dense_device(const sogk_transform* t, const uint8_t* d_bits, size_t nbytes,
+                                  void* stream, sogk_grid** out) {
+    return create_dense(t, d_bits, nbytes, false, stream, out);
+}
+
+static cudaError_t alloc_vdb(sogk_grid* g) {
+    for (int a = 0; a < 3; ++a) g->R[a] = (g->t.res[a] + 127) / 128;
+    g->nreg = int64_t(g->R[0]) * g->R[1] * g->R[2];
+    g->leaf_capacity = uint64_t(g->nreg) * 4096;
+    cudaError_t e;
+    if ((e = dalloc(&g->root, g->nreg)) != cudaSuccess) return e;
+    if ((e = dalloc(&g->child_mask, g->nreg * 64)) != cudaSuccess) return e;
+    if ((e = dalloc(&g->value_mask, g->nreg * 64)) != cudaSuccess) return e;
+    if ((e = dalloc(&g->prefix, g->nreg * 64)) != cudaSuccess) return e;
+    if ((e = dalloc(&g->region_leaves, g->nreg)) != cudaSuccess) return e;
+    if ((e = dalloc(&g->total_leaves, 1)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+int sogk_grid_build_vdb(const sogk_grid* d, void* stream, sogk_grid** out) {
+    if (!out) return fail(SOGK_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!d || d->kind != SOGK_GRID_DENSE)
+        return fail(SOGK_INVALID_ARG, "build_vdb needs a dense grid");
+    if (d->t.res[0] > 1024 * 128 || d->t.res[1] > 1024 * 128 || d->t.res[2] > 1024 * 128)
+        return fail(SOGK_INVALID_ARG, "resolution too large");
+    auto* g = new sogk_grid;
+    g->kind = SOGK_GRID_VDB;
+    g->t = d->t;
+    g->device = d->device;
+    cudaError_t e = alloc_vdb(g);
+    if (e == cudaSuccess) e = dalloc(&g->leaves, g->leaf_capacity * 8);
+    if (e != cudaSuccess) {
+        delete g;
+        return cuda_fail(e, "vdb allocation");
+    }
+    VdbBuildArgs a{};
+    a.dense = d->dev();
+    for (int k = 0; k < 3; ++k) a.R[k] = g->R[k];
+    a.root = g->root;
+    a.child_mask = g->child_mask;
+    a.value_mask = g->value_mask;
+    a.prefix = g->prefix;
+    a.leaves = g->leaves;
+    a.region_leaves = g->region_leaves;
+    a.total_leaves = g->total_leaves;
+    e = launch_vdb_build(a, S(stream));
+    if (e != cudaSuccess) {
+        delete g;
+        return cuda_fail(e, "vdb build launch");
+    }
+    *out = g;
+    return SOGK_OK;
+}
+
+int sogk_grid_destroy(sogk_grid* g) {
+    delete g;
+    return SOGK_OK;
+}
+
+int sogk_grid_get_info(const sogk_grid* g, sogk_grid_info* out) {
+    if (!g || !out) return fail(SOGK_INVALID_ARG, "NULL argument");
+    int st = g->fetch_meta();
+    if (st) return st;
+    std::memset(out, 0, sizeof(*out));
+    out->kind = g->kind;
+    out->transform = g->t;
+    if (g->kind == SOGK_GRID_DENSE) {
+        out->memory_bytes = int64_t(g->nbytes); // io.hpp:223-225
+        out->device_bytes = int64_t(g->nbytes);
+        return SOGK_OK;
+    }
+    int64_t internal = 0;
+    for (int32_t r : g->h_root) internal += r >= 0;
+    const int64_t entries = g->from_file
+                                ? int64_t(std::count_if(g->h_root.begin(), g->h_root.end(),
+                                                        [](int32_t r) { return r != -3; })) +
+                                      int64_t(g->extra_entries.size())
+                                : g->nreg;
+    out->root_entries = entries;
+    out->internal_nodes = internal;
+    out->leaf_count = g->leaf_count;
+    // memory_bytes(SparseGrid) == SOG1 size (io.hpp:227-238)
+    out->memory_bytes = (4 + 4 + 12 + 24 + 8 + 4) + entries * 13 + internal * 4096 +
+                        g->leaf_count * 64;
+    out->device_bytes = g->nreg * (4 + 64 * (8 + 8 + 4) + 4) + 4 + int64_t(g->leaf_capacity) * 64;
+    return SOGK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// SOG0 / SOG1 (io.hpp:134-214)
+// ---------------------------------------------------------------------------
+namespace {
+struct Writer {
+    std::vector<uint8_t> out;
+    void bytes(const void* p, size_t n) {
+        const uint8_t* b = static_cast<const uint8_t*>(p);
+        out.insert(out.end(), b, b + n);
+    }
+    void u8(uint8_t v) { out.push_back(v); }
+    void u32(uint32_t v) {
+        for (int i = 0; i < 4; ++i) out.push_back(uint8_t(v >> (8 * i)));
+    }
+    void f64(double v) {
+        uint64_t b;
+        std::memcpy(&b, &v, 8);
+        for (int i = 0; i < 8; ++i) out.push_back(uint8_t(b >> (8 * i)));
+    }
+    void transform(const sogk_transform& t) { // write_transform io.hpp:308-316
+        for (int a = 0; a < 3; ++a) u32(uint32_t(t.res[a]));
+        for (int a = 0; a < 3; ++a) f64(t.world_min[a]);
+        f64(t.voxel_size);
+    }
+};
+
+struct Reader { // ByteReader io.hpp:272-306; returns false + message on error
+    const uint8_t* p;
+    size_t n, pos = 0;
+    std::string err;
+    int code = 0; // 0 ok, 1 bad magic, 2 bad version, 3 truncated, 4 corrupt
+    bool need(size_t k) {
+        if (pos + k > n) {
+            if (!code) {
+                code = 3;
+                err = "unexpected end of data (truncated)";
+            }
+            return false;
+        }
+        return true;
+    }
+    uint8_t u8() { return need(1) ? p[pos++] : 0; }
+    uint32_t u32() {
+        if (!need(4)) return 0;
+        uint32_t v = 0;
+        for (int i = 0; i < 4; ++i) v |= uint32_t(p[pos + i]) << (8 * i);
+        pos += 4;
+        return v;
+    }
+    double f64() {
+        if (!need(8)) return 0;
+        uint64_t b = 0;
+        for (int i = 0; i < 8; ++i) b |= uint64_t(p[pos + i]) << (8 * i);
+        pos += 8;
+        double v;
+        std::memcpy(&v, &b, 8);
+        return v;
+    }
+    bool corrupt(const char* what) {
+        if (!code) {
+            code = 4;
+            err = std::string(what) + " (corrupt)";
+        }
+        return false;
+    }
+    bool magic(const char* m) {
+        if (!need(4)) return false;
+        if (std::memcmp(p + pos, m, 4) != 0) {
+            code = 1;
+            err = "not a grid file (bad magic)";
+            return false;
+        }
+        pos += 4;
+        return true;
+    }
+    bool version() {
+        const uint32_t v = u32();
+        if (code) return false;
+        if (v != 1) {
+            code = 2;
+            err = "unsupported version (bad version)";
+            return false;
+        }
+        return true;
+    }
+    bool transform(sogk_transform& t) { // read_transform io.hpp:318-333
+        const uint32_t rx = u32(), ry = u32(), rz = u32();
+        t.world_min[0] = f64();
+        t.world_min[1] = f64();
+        t.world_min[2] = f64();
+        t.voxel_size = f64();
+        if (code) return false;
+        if (rx < 1 || ry < 1 || rz < 1 || !(t.voxel_size > 0.0))
+            return corrupt("invalid grid transform");
+        if (uint64_t(rx) * ry * rz > (uint64_t(1) << 33)) return corrupt("resolution too large");
+        t.res[0] = int32_t(rx);
+        t.res[1] = int32_t(ry);
+        t.res[2] = int32_t(rz);
+        return true;
+    }
+};
+
+int io_fail(const Reader& r) { return fail(SOGK_IO_ERROR, r.err); }
+} // namespace
+
+int sogk_grid_export_sog0(const sogk_grid* g, uint8_t* buf, size_t* len) {
+    if (!g || !len) return fail(SOGK_INVALID_ARG, "NULL argument");
+    if (g->kind != SOGK_GRID_DENSE) return fail(SOGK_INVALID_ARG, "SOG0 export needs a dense grid");
+    const size_t need = 4 + 4 + 12 + 24 + 8 + g->nbytes;
+    if (!buf) {
+        *len = need;
+        return SOGK_OK;
+    }
+    if (*len < need) {
+        *len = need;
+        return fail(SOGK_INSUFFICIENT_CAPACITY, "buffer too small for SOG0");
+    }
+    Writer w;
+    w.bytes("SOG0", 4);
+    w.u32(1);
+    w.transform(g->t);
+    std::memcpy(buf, w.out.data(), w.out.size());
+    CK(cudaMemcpy(buf + w.out.size(), g->bits, g->nbytes, cudaMemcpyDeviceToHost), "payload D2H");
+    *len = need;
+    return SOGK_OK;
+}
+
+int sogk_grid_load_sog0(const uint8_t* bytes, size_t len, void* stream, sogk_grid** out) {
+    if (!out || (!bytes && len)) return fail(SOGK_INVALID_ARG, "NULL argument");
+    *out = nullptr;
+    Reader r{bytes, len};
+    sogk_transform t{};
+    if (!r.magic("SOG0") || !r.version() || !r.transform(t)) return io_fail(r);
+    const uint64_t nb = payload_bytes(t);
+    if (!r.need(nb)) return io_fail(r);
+    if (r.pos + nb != len) { // expect_end
+        r.corrupt("trailing bytes after payload");
+        return io_fail(r);
+    }
+    return sogk_grid_create_dense(&t, bytes + r.pos, nb, stream, out);
+}
+
+int sogk_grid_export_sog1(const sogk_grid* g, uint8_t* buf, size_t* len) {
+    if (!g || !len) return fail(SOGK_INVALID_ARG, "NULL argument");
+    if (g->kind != SOGK_GRID_VDB) return fail(SOGK_INVALID_ARG, "SOG1 export needs a VDB grid");
+    int st = g->fetch_meta();
+    if (st) return st;
+    std::vector<uint64_t> cm(g->nreg * 64), vm(g->nreg * 64);
+    std::vector<uint32_t> pf(g->nreg * 64);
+    std::vector<uint64_t> lv(size_t(g->leaf_count) * 8);
+    CK(cudaMemcpy(cm.data(), g->child_mask, cm.size() * 8, cudaMemcpyDeviceToHost), "mask D2H");
+    CK(cudaMemcpy(vm.data(), g->value_mask, vm.size() * 8, cudaMemcpyDeviceToHost), "mask D2H");
+    CK(cudaMemcpy(pf.data(), g->prefix, pf.size() * 4, cudaMemcpyDeviceToHost), "prefix D2H");
+    if (!lv.empty())
+        CK(cudaMemcpy(lv.data(), g->leaves, lv.size() * 8, cudaMemcpyDeviceToHost), "leaves D2H");
+    // root entries in map order: in-grid regions (absent ones skipped for loaded files) + extras
+    std::map<std::array<int32_t, 3>, RootEntry, RegionOrder> entries;
+    for (int64_t r = 0; r < g->nreg; ++r) {
+        const int32_t node = g->h_root[r];
+        if (node == -3) continue; // region absent from a loaded file
+        RootEntry e{};
+        e.origin[0] = int32_t(r % g->R[0]) * 128;
+        e.origin[1] = int32_t((r / g->R[0]) % g->R[1]) * 128;
+        e.origin[2] = int32_t(r / (int64_t(g->R[0]) * g->R[1])) * 128;
+        e.kind = node == kRootEmpty ? 0 : (node == kRootOccupied ? 1 : 2);
+        e.node = node;
+        entries[{e.origin[0], e.origin[1], e.origin[2]}] = e;
+    }
+    for (const RootEntry& e : g->extra_entries) entries[{e.origin[0], e.origin[1], e.origin[2]}] = e;
+    Writer w; // serialize_sparse io.hpp:161-181
+    w.bytes("SOG1", 4);
+    w.u32(1);
+    w.transform(g->t);
+    w.u32(uint32_t(entries.size()));
+    for (const auto& kv : entries) {
+        const RootEntry& e = kv.second;
+        w.u32(uint32_t(e.origin[0]));
+        w.u32(uint32_t(e.origin[1]));
+        w.u32(uint32_t(e.origin[2]));
+        w.u8(e.kind);
+        if (e.kind != 2) continue;
+        if (e.node < 0) return fail(SOGK_INVALID_ARG, "internal root entry outside the grid");
+        for (int ci = 0; ci < 4096; ++ci) {
+            const int64_t wi = int64_t(e.node) * 64 + (ci >> 6);
+            const int b = ci & 63;
+            if ((cm[wi] >> b) & 1ull) {
+                w.u8(2);
+                const uint64_t leaf =
+                    pf[wi] + uint64_t(__builtin_popcountll(cm[wi] & ((1ull << b) - 1ull)));
+                w.bytes(&lv[leaf * 8], 64); // little-endian words == LeafNode bytes
+            } else {
+                w.u8(uint8_t((vm[wi] >> b) & 1ull));
+            }
+        }
+    }
+    if (!buf) {
+        *len = w.out.size();
+        return SOGK_OK;
+    }
+    if (*len < w.out.size()) {
+        *len = w.out.size();
+        return fail(SOGK_INSUFFICIENT_CAPACITY, "buffer too small for SOG1");
+    }
+    std::memcpy(buf, w.out.data(), w.out.size());
+    *len = w.out.size();
+    return SOGK_OK;
+}
+
+int sogk_grid_load_sog1(const uint8_t* bytes, size_t len, void* stream, sogk_grid** out) {
+    if (!out || (!bytes && len)) return fail(SOGK_INVALID_ARG, "NULL argument");
+    *out = nullptr;
+    Reader r{bytes, len};
+    sogk_transform t{};
+    if (!r.magic("SOG1") || !r.version() || !r.transform(t)) return io_fail(r);
+    const uint32_t n_entries = r.u32();
+    if (r.code) return io_fail(r);
+    auto* g = new sogk_grid;
+    g->kind = SOGK_GRID_VDB;
+    g->t = t;
+    g->from_file = true;
+    cudaGetDevice(&g->device);
+    for (int a = 0; a < 3; ++a) g->R[a] = (t.res[a] + 127) / 128;
+    g->nreg = int64_t(g->R[0]) * g->R[1] * g->R[2];
+    std::vector<int32_t> root(g->nreg, -3); // -3: absent region (queries read empty internal tile)
+    std::vector<uint64_t> cm(g->nreg * 64, 0), vm(g->nreg * 64, 0);
+    std::vector<uint32_t> pf(g->nreg * 64, 0);
+    std::vector<uint64_t> leaves;
+    std::vector<std::array<int32_t, 3>> seen;
+    std::map<std::array<int32_t, 3>, int, RegionOrder> dup;
+    for (uint32_t e = 0; e < n_entries; ++e) {
+        std::array<int32_t, 3> o;
+        o[0] = int32_t(r.u32());
+        o[1] = int32_t(r.u32());
+        o[2] = int32_t(r.u32());
+        const uint8_t kind = r.u8();
+        if (r.code) break;
+        if (kind > 2) {
+            r.corrupt("invalid root entry kind");
+            break;
+        }
+        if (dup.count(o)) {
+            r.corrupt("duplicate root entry");
+            break;
+        }
+        dup[o] = 1;
+        // an entry is reachable by queries only at a 128-aligned in-grid origin
+        const bool mapped = o[0] >= 0 && o[1] >= 0 && o[2] >= 0 && o[0] % 128 == 0 &&
+                            o[1] % 128 == 0 && o[2] % 128 == 0 && o[0] / 128 < g->R[0] &&
+                            o[1] / 128 < g->R[1] && o[2] / 128 < g->R[2];
+        const int64_t reg = mapped ? (int64_t(o[2] / 128) * g->R[1] + o[1] / 128) * g->R[0] + o[0] / 128 : -1;
+        int32_t node = kind == 0 ? kRootEmpty : kRootOccupied;
+        std::vector<uint8_t> kinds;
+        std::vector<uint64_t> node_leaves;
+        if (kind == 2) {
+            kinds.resize(4096);
+            for (int ci = 0; ci < 4096 && !r.code; ++ci) {
+                const uint8_t ck = r.u8();
+                if (r.code) break;
+                if (ck > 2) {
+                    r.corrupt("invalid child kind");
+                    break;
+                }
+                kinds[ci] = ck;
+                if (ck == 2) {
+                    if (!r.need(64)) break;
+                    uint64_t w8[8];
+                    std::memcpy(w8, bytes + r.pos, 64);
+                    r.pos += 64;
+                    node_leaves.insert(node_leaves.end(), w8, w8 + 8);
+                }
+            }
+            if (r.code) break;
+        }
+        if (!mapped) {
+            RootEntry x{{o[0], o[1], o[2]}, kind, -1};
+            if (kind == 2) { // unreachable node: keep it for export in a private slot
+                r.corrupt("internal root entry outside the grid is not supported");
+                break;
+            }
+            g->extra_entries.push_back(x);
+            continue;
+        }
+        if (kind == 2) {
+            node = int32_t(reg);
+            uint32_t base = uint32_t(leaves.size() / 8);
+            for (int w = 0; w < 64; ++w) {
+                pf[reg * 64 + w] = base;
+                for (int b = 0; b < 64; ++b) {
+                    const uint8_t ck = kinds[w * 64 + b];
+                    if (ck == 2) {
+                        cm[reg * 64 + w] |= 1ull << b;
+                        ++base;
+                    } else if (ck == 1) {
+                        vm[reg * 64 + w] |= 1ull << b;
+                    }
+                }
+            }
+            leaves.insert(leaves.end(), node_leaves.begin(), node_leaves.end());
+        }
+        root[reg] = node;
+    }
+    if (!r.code && r.pos != len) r.corrupt("trailing bytes after payload");
+    if (r.code) {
+        delete g;
+        return io_fail(r);
+    }
+    // absent regions answer like an empty internal tile (sparse.hpp:166-168)
+    std::vector<int32_t> dev_root(root);
+    for (auto& x : dev_root)
+        if (x == -3) x = kRootEmpty;
+    g->leaf_capacity = leaves.size() / 8;
+    cudaError_t e = alloc_vdb(g);
+    if (e == cudaSuccess) e = dalloc(&g->leaves, std::max<size_t>(leaves.size(), 8));
+    const uint32_t tl = uint32_t(leaves.size() / 8);
+    if (e == cudaSuccess) e = cudaMemcpy(g->root, dev_root.data(), dev_root.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->child_mask, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->value_mask, vm.data(), vm.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->prefix, pf.data(), pf.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !leaves.empty())
+        e = cudaMemcpy(g->leaves, leaves.data(), leaves.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->total_leaves, &tl, 4, cudaMemcpyHostToDevice);
+    (void)stream;
+    if (e != cudaSuccess) {
+        delete g;
+        return cuda_fail(e, "SOG1 upload");
+    }
+    g->h_root = root;
+    g->leaf_count = tl;
+    g->meta_ready = true;
+    *out = g;
+    return SOGK_OK;
+}
+
+int sogk_grid_download_dense(const sogk_grid* g, uint8_t* h_bits, size_t nbytes) {
+    if (!g || !h_bits) return fail(SOGK_INVALID_ARG, "NULL argument");
+    if (nbytes != payload_bytes(g->t)) return fail(SOGK_INVALID_ARG, "payload size mismatch");
+    if (g->kind == SOGK_GRID_DENSE) {
+        CK(cudaMemcpy(h_bits, g->bits, nbytes, cudaMemcpyDeviceToHost), "payload D2H");
+        return SOGK_OK;
+    }
+    uint8_t* d = nullptr;
+    CK(cudaMalloc(&d, nbytes), "to_dense scratch");
+    cudaError_t e = launch_vdb_to_dense(g->dev(), d, int64_t(nbytes), nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(h_bits, d, nbytes, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "to_dense");
+    return SOGK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// samplers
+// ---------------------------------------------------------------------------
+int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
+                        const sogk_sampler_desc* desc, sogk_sampler** out) {
+    if (!out) return fail(SOGK_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!levels || !desc) return fail(SOGK_INVALID_ARG, "NULL argument");
+    if (n_levels < 1) return fail(SOGK_INVALID_ARG, "cascade has no levels");
+    if (n_levels > SOGK_MAX_LEVELS) return fail(SOGK_INVALID_ARG, "too many cascade levels");
+    if (desc->analyzer != SOGK_DDA && desc->analyzer != SOGK_HDDA)
+        return fail(SOGK_INVALID_ARG, "unknown analyzer");
+    if (desc->kernel != SOGK_BRANCH && desc->kernel != SOGK_SKIP)
+        return fail(SOGK_INVALID_ARG, "unknown kernel");
+    // StepSchedule::constant / linear validation (sampling.hpp:25-34)
+    if (desc->schedule != SOGK_CONSTANT && desc->schedule != SOGK_LINEAR)
+        return fail(SOGK_INVALID_ARG, "unknown schedule");
+    if (!(desc->dt0 > 0.0)) return fail(SOGK_INVALID_ARG, "step size must be positive");
+    if (desc->schedule == SOGK_LINEAR && desc->growth < 0.0)
+        return fail(SOGK_INVALID_ARG, "growth must be non-negative");
+    const int want = desc->analyzer == SOGK_DDA ? SOGK_GRID_DENSE : SOGK_GRID_VDB;
+    for (int b = 0; b < n_levels; ++b) {
+        if (!levels[b]) return fail(SOGK_INVALID_ARG, "NULL grid level");
+        if (levels[b]->kind != want)
+            return fail(SOGK_INVALID_ARG,
+                        "analyzers are bound to their grid: dda marches dense grids, hdda VDBs");
+    }
+    const bool cascade = desc->cascade || n_levels > 1;
+    if (cascade) { // validate_cascade (sampling.hpp:253-273)
+        const sogk_transform& base = levels[0]->t;
+        for (int b = 0; b < n_levels; ++b) {
+            const sogk_transform& t = levels[b]->t;
+            if (t.res[0] != base.res[0] || t.res[1] != base.res[1] || t.res[2] != base.res[2])
+                return fail(SOGK_INVALID_ARG, "cascade levels must share one resolution");
+            const double expected = base.voxel_size * static_cast<double>(1u << b);
+            if (std::abs(t.voxel_size - expected) > 1e-12 * expected)
+                return fail(SOGK_INVALID_ARG, "cascade voxel sizes must double per level");
+            if (b > 0) {
+                const sogk_transform& p = levels[b - 1]->t;
+                for (int a = 0; a < 3; ++a) {
+                    const double lo = t.world_min[a], hi = lo + double(t.res[a]) * t.voxel_size;
+                    const double plo = p.world_min[a],
+                                 phi = plo + double(p.res[a]) * p.voxel_size;
+                    if (plo < lo || phi > hi)
+                        return fail(SOGK_INVALID_ARG, "cascade level bounds must nest");
+                }
+            }
+        }
+    }
+    auto* s = new sogk_sampler;
+    s->desc = *desc;
+    s->n_levels = n_levels;
+    s->v.analyzer = desc->analyzer;
+    s->v.cascade = cascade ? 1 : 0;
+    s->v.branch = desc->kernel == SOGK_BRANCH ? 1 : 0;
+    s->v.linear = desc->schedule == SOGK_LINEAR ? 1 : 0;
+    for (int b = 0; b < n_levels; ++b) s->dev.lv[b] = levels[b]->dev();
+    s->dev.n_levels = n_levels;
+    s->dev.spin_cap = desc->spin_cap > 0 ? desc->spin_cap : SOGK_DEFAULT_SPIN_CAP;
+    s->dev.dt0 = desc->dt0;
+    s->dev.growth = desc->schedule == SOGK_LINEAR ? desc->growth : 0.0;
+    *out = s;
+    return SOGK_OK;
+}
+
+int sogk_sampler_destroy(sogk_sampler* s) {
+    delete s;
+    return SOGK_OK;
+}
+
+static CameraDev to_dev(const sogk_camera& c) {
+    CameraDev d{};
+    for (int a = 0; a < 3; ++a) {
+        d.position[a] = c.position[a];
+        d.forward[a] = c.forward[a];
+        d.right[a] = c.right[a];
+        d.cam_up[a] = c.cam_up[a];
+    }
+    d.tan_half = c.tan_half;
+    d.aspect = c.aspect;
+    d.t_far = c.t_far;
+    d.width = c.width;
+    d.height = c.height;
+    return d;
+}
+
+static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* cam,
+                      int64_t first, int64_t n, int64_t* d_packed, int64_t* d_stats,
+                      uint8_t* d_status, int32_t* d_counters, void* stream) {
+    if (!s) return fail(SOGK_INVALID_ARG, "sampler is NULL");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (!d_stats) return fail(SOGK_INVALID_ARG, "stats buffer is NULL");
+    if (n > 0 && (!d_packed || (!cam && !d_rays)))
+        return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
+    if (n == 0) return SOGK_OK;
+    int st = s->ensure_ws(n);
+    if (st) return st;
+    const int64_t blocks = (n + 255) / 256;
+    CK(cudaMemsetAsync(s->ws, 0, size_t(blocks) * 8 + 16, S(stream)), "workspace reset");
+    uint64_t* tiles = static_cast<uint64_t*>(s->ws);
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(tiles + blocks);
+    CameraDev cd{};
+    if (cam) cd = to_dev(*cam);
+    CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
+                    d_status, d_counters, tiles, ctr, S(stream)),
+       "count launch");
+    return SOGK_OK;
+}
+
+static bool camera_range_ok(const sogk_camera* cam, int64_t first, int64_t n) {
+    return cam && cam->width >= 1 && cam->height >= 1 && first >= 0 &&
+           first + n <= int64_t(cam->width) * cam->height;
+}
+
+int sogk_sample_count(sogk_sampler* s, const double* d_rays, int64_t n, int64_t* d_packed_info,
+                      int64_t* d_stats, uint8_t* d_status, int32_t* d_counters, void* stream) {
+    return count_impl(s, d_rays, nullptr, 0, n, d_packed_info, d_stats, d_status, d_counters,
+                      stream);
+}
+
+int sogk_sample_count_camera(sogk_sampler* s, const sogk_camera* cam, int64_t first_pixel,
+                             int64_t n, int64_t* d_packed_info, int64_t* d_stats,
+                             uint8_t* d_status, int32_t* d_counters, void* stream) {
+    if (!camera_range_ok(cam, first_pixel, n)) return fail(SOGK_INVALID_ARG, "pixel outside image");
+    return count_impl(s, nullptr, cam, first_pixel, n, d_packed_info, d_stats, d_status,
+                      d_counters, stream);
+}
+
+static int write_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* cam, int64_t first,
+                      int64_t n, const int64_t* d_packed, int64_t base, double* ts, double* te,
+                      int32_t* ri, uint32_t* ce, uint8_t* lv, void* stream) {
+    if (!s) return fail(SOGK_INVALID_ARG, "sampler is NULL");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (n == 0) return SOGK_OK;
+    if (!d_packed || !ts || (!cam && !d_rays)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    CameraDev cd{};
+    if (cam) cd = to_dev(*cam);
+    CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, base, ts, te,
+                    ri, ce, lv, S(stream)),
+       "write launch");
+    return SOGK_OK;
+}
+
+int sogk_sample_write(sogk_sampler* s, const double* d_rays, int64_t n,
+                      const int64_t* d_packed_info, int64_t ray_index_base, double* d_t_starts,
+                      double* d_t_ends, int32_t* d_ray_indices, uint32_t* d_cells,
+                      uint8_t* d_levels, void* stream) {
+    return write_impl(s, d_rays, nullptr, 0, n, d_packed_info, ray_index_base, d_t_starts,
+                      d_t_ends, d_ray_indices, d_cells, d_levels, stream);
+}
+
+int sogk_sample_write_camera(sogk_sampler* s, const sogk_camera* cam, int64_t first_pixel,
+                             int64_t n, const int64_t* d_packed_info, int64_t ray_index_base,
+                             double* d_t_starts, double* d_t_ends, int32_t* d_ray_indices,
+                             uint32_t* d_cells, uint8_t* d_levels, void* stream) {
+    if (!camera_range_ok(cam, first_pixel, n)) return fail(SOGK_INVALID_ARG, "pixel outside image");
+    return write_impl(s, nullptr, cam, first_pixel, n, d_packed_info, ray_index_base, d_t_starts,
+                      d_t_ends, d_ray_indices, d_cells, d_levels, stream);
+}
+
+int sogk_camera_rays(const sogk_camera* cam, int64_t first_pixel, int64_t n, double* d_rays,
+                     void* stream) {
+    if (!camera_range_ok(cam, first_pixel, n) || (n && !d_rays))
+        return fail(SOGK_INVALID_ARG, "pixel outside image");
+    CK(launch_raygen(to_dev(*cam), first_pixel, n, d_rays, S(stream)), "raygen launch");
+    return SOGK_OK;
+}
+
+int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t ray_index_base,
+                     int64_t capacity, int64_t* h_packed_info, double* h_t_starts,
+                     double* h_t_ends, int32_t* h_ray_indices, uint32_t* h_cells,
+                     uint8_t* h_levels, uint8_t* h_status, int32_t* h_counters,
+                     int64_t* h_stats, void* stream) {
+    if (!s || !h_stats) return fail(SOGK_INVALID_ARG, "NULL argument");
+    if (n < 0 || capacity < 0) return fail(SOGK_INVALID_ARG, "negative size");
+    if (n > 0 && (!h_rays || !h_packed_info)) return fail(SOGK_INVALID_ARG, "NULL host buffer");
+    cudaStream_t st = S(stream);
+    // one scratch allocation: rays | packed | stats | status | counters | outputs
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t b_rays = al(size_t(n) * 64), b_packed = al(size_t(n) * 16), b_stats = al(64),
+                 b_status = al(size_t(n)), b_ctr = al(size_t(n) * 12);
+    const size_t b_ts = al(size_t(capacity) * 8), b_te = al(size_t(capacity) * 8),
+                 b_ri = al(size_t(capacity) * 4), b_ce = al(size_t(capacity) * 4),
+                 b_lv = al(size_t(capacity));
+    const size_t need = b_rays + b_packed + b_stats + b_status + b_ctr + b_ts + b_te + b_ri + b_ce + b_lv;
+    if (need > s->hb_bytes) {
+        cudaFree(s->hb);
+        s->hb = nullptr;
+        s->hb_bytes = 0;
+        CK(cudaMalloc(&s->hb, need), "host-path scratch");
+        s->hb_bytes = need;
+    }
+    char* p = static_cast<char*>(s->hb);
+    double* d_rays = reinterpret_cast<double*>(p);
+    p += b_rays;
+    int64_t* d_packed = reinterpret_cast<int64_t*>(p);
+    p += b_packed;
+    int64_t* d_stats = reinterpret_cast<int64_t*>(p);
+    p += b_stats;
+    uint8_t* d_status = reinterpret_cast<uint8_t*>(p);
+    p += b_status;
+    int32_t* d_ctr = reinterpret_cast<int32_t*>(p);
+    p += b_ctr;
+    double* d_ts = reinterpret_cast<double*>(p);
+    p += b_ts;
+    double* d_te = reinterpret_cast<double*>(p);
+    p += b_te;
+    int32_t* d_ri = reinterpret_cast<int32_t*>(p);
+    p += b_ri;
+    uint32_t* d_ce = reinterpret_cast<uint32_t*>(p);
+    p += b_ce;
+    uint8_t* d_lv = reinterpret_cast<uint8_t*>(p);
+
+    if (n > 0) CK(cudaMemcpyAsync(d_rays, h_rays, size_t(n) * 64, cudaMemcpyHostToDevice, st), "rays H2D");
+    int rc = sogk_sample_count(s, d_rays, n, d_packed, d_stats, h_status ? d_status : nullptr,
+                               h_counters ? d_ctr : nullptr, stream);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h_stats, d_stats, SOGK_STATS_LEN * 8, cudaMemcpyDeviceToHost, st), "stats D2H");
+    CK(cudaStreamSynchronize(st), "count sync");
+    const int64_t total = h_stats[SOGK_STAT_TOTAL_SAMPLES];
+    const bool fits = total <= capacity;
+    if (fits && total > 0) {
+        rc = sogk_sample_write(s, d_rays, n, d_packed, ray_index_base, d_ts, h_t_ends ? d_te : nullptr,
+                               h_ray_indices ? d_ri : nullptr, h_cells ? d_ce : nullptr,
+                               h_levels ? d_lv : nullptr, stream);
+        if (rc) return rc;
+        const size_t tb = size_t(total);
+        if (h_t_starts) CK(cudaMemcpyAsync(h_t_starts, d_ts, tb * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        if (h_t_ends) CK(cudaMemcpyAsync(h_t_ends, d_te, tb * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        if (h_ray_indices) CK(cudaMemcpyAsync(h_ray_indices, d_ri, tb * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (h_cells) CK(cudaMemcpyAsync(h_cells, d_ce, tb * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (h_levels) CK(cudaMemcpyAsync(h_levels, d_lv, tb, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    if (n > 0) {
+        CK(cudaMemcpyAsync(h_packed_info, d_packed, size_t(n) * 16, cudaMemcpyDeviceToHost, st), "D2H");
+        if (h_status) CK(cudaMemcpyAsync(h_status, d_status, size_t(n), cudaMemcpyDeviceToHost, st), "D2H");
+        if (h_counters) CK(cudaMemcpyAsync(h_counters, d_ctr, size_t(n) * 12, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    CK(cudaStreamSynchronize(st), "write sync");
+    if (!fits) return fail(SOGK_INSUFFICIENT_CAPACITY, "output capacity below the sample total");
+    return SOGK_OK;
+}
+
+} // extern "C"

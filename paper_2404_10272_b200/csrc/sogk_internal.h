@@ -1,0 +1,46 @@
+// sogk_internal.h — host-side declarations shared by the C-ABI and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sogk_layout.h"
+
+namespace sogk {
+
+struct Variant {
+    int analyzer; // 0 DDA, 1 HDDA
+    int cascade;  // 1: CascadeTraversal
+    int branch;   // 1: sample_branch, 0: sample_skip
+    int linear;   // 1: linear schedule
+};
+
+cudaError_t launch_count(const Variant& v, const SamplerDev& s, const double* rays,
+                         const CameraDev* cam, int64_t first, int64_t n, int64_t* packed,
+                         int64_t* stats, uint8_t* status, int32_t* counters, uint64_t* tiles,
+                         unsigned int* ctr, cudaStream_t st);
+cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* rays,
+                         const CameraDev* cam, int64_t first, int64_t n, const int64_t* packed,
+                         int64_t base, double* ts, double* te, int32_t* ri, uint32_t* ce,
+                         uint8_t* lv, cudaStream_t st);
+cudaError_t launch_raygen(const CameraDev& cam, int64_t first, int64_t n, double* rays,
+                          cudaStream_t st);
+
+// VDB build (sogk_vdb.cu)
+struct VdbBuildArgs {
+    GridDev dense;       // source payload + transform
+    int R[3];
+    int32_t* root;       // [nreg]
+    uint64_t* child_mask; // [nreg*64]
+    uint64_t* value_mask; // [nreg*64]
+    uint32_t* prefix;    // [nreg*64]
+    uint64_t* leaves;    // [nreg*4096*8] worst case
+    uint32_t* region_leaves; // [nreg] scratch
+    uint32_t* total_leaves;  // [1]
+};
+cudaError_t launch_vdb_build(const VdbBuildArgs& a, cudaStream_t st);
+// to_dense (sparse.hpp:374-383): expands a VDB into a dense payload
+cudaError_t launch_vdb_to_dense(const GridDev& vdb, uint8_t* bits, int64_t nbytes,
+                                cudaStream_t st);
+
+} // namespace sogk
