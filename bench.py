@@ -1,0 +1,603 @@
+#!/usr/bin/env python3
+"""bench.py — rays/s and samples/s of the B200 VDB+HDDA sampler (arXiv 2404.10272 hot path).
+
+Default workload = BASELINE.json configs[1], "NeRF-Synthetic-shaped sweep": 8 procedural
+128^3 object grids of varying sparsity (SURVEY §8d cfg 2), 200 views of 800x800 each on
+an orbit through the bench camera pose (1.9, 1.4, 2.3) -> 0, vfov 42 deg.  One step = one
+view of each of the 8 objects (8 x 640,000 rays), sharded over ranks by view (weak
+scaling: every rank does one view per object per step).  Per object and step the product
+path runs pass 1 (count + fused scan) and pass 2 (write) of `sparse+hdda+skip` through the
+C-ABI; the paper's dense baseline `dense+dda+branch` (and its skip twin) is timed the same
+way.  Rays are materialized in HBM before the timed region (distinct per object and step:
+328 MB of rays + ~1-2 GB of samples per step > the 126 MB L2, so no explicit L2 flush).
+
+JSON line keys follow the driver contract; see DESIGN.md §Measurement for the roofline basis.
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg3|cfg4]
+  python bench.py --impl reference ...   (the reference CPU sampler on the host cores)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CAM_POS = (1.9, 1.4, 2.3)
+N_VIEWS = 200
+
+# cfg 2: 8 procedural 128^3 objects of varying sparsity
+CFG2_OBJECTS = [
+    ("shell", dict(seed=1, count=12)),
+    ("shell", dict(seed=2, count=256)),
+    ("blobs", dict(seed=1, count=6)),
+    ("blobs", dict(seed=2, count=12)),
+    ("blobs", dict(seed=3, count=24)),
+    ("blobs", dict(seed=4, count=48)),
+    ("sponge", dict(seed=1)),
+    ("random", dict(seed=1, fraction=0.02)),
+]
+
+
+def orbit_camera(P, view: int, width=800, height=800):
+    """View v of the orbit: the bench pose rotated about +y by 2*pi*v/200 (v = 0 is cfg 1)."""
+    th = 2.0 * math.pi * (view % N_VIEWS) / N_VIEWS
+    x, y, z = CAM_POS
+    pos = (x * math.cos(th) + z * math.sin(th), y, -x * math.sin(th) + z * math.cos(th))
+    return P.Camera(pos, (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, width, height)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+class Workload:
+    """Grids (per object) + a ray generator per (step, object) + the schedule."""
+
+    def __init__(self, P, name: str):
+        self.P, self.name = P, name
+        base = P.GridTransform.cube(128, (-1.0, -1.0, -1.0), 2.0)
+        self.cascade = False
+        self.schedule = P.StepSchedule.constant(0.5 * base.voxel_size)
+        if name == "cfg2":
+            self.objects = []
+            for kind, kw in CFG2_OBJECTS:
+                bits, occ = P.generate_scene(kind, base, **kw)
+                self.objects.append(dict(label=f"{kind}:{kw}", levels=[(base, bits)], occupancy=occ))
+            self.width = self.height = 800
+            self.desc = ("8 procedural 128^3 objects (shell s1, shell s2 n256, blobs s1..s4 n6..48, "
+                         "sponge s1, random 2%), 800x800 orbit views, dt0 = half voxel")
+        elif name == "cfg1":
+            bits, occ = P.generate_scene("shell", base, seed=1)
+            self.objects = [dict(label="shell s1", levels=[(base, bits)], occupancy=occ)]
+            self.width = self.height = 800
+            self.desc = "single-level 128^3 shell s1, 800x800 bench camera, dt0 = half voxel"
+        elif name == "cfg3":
+            lv = P.build_dense_cascade("blobs", base, 4, seed=1)
+            self.objects = [dict(label="blobs s1 x4 cascade", levels=lv, occupancy=None)]
+            self.cascade = True
+            self.width, self.height = 1297, 840
+            self.schedule = P.StepSchedule.linear(0.5 * base.voxel_size, 1.0 / 256.0)
+            self.desc = "4-level 128^3 blobs s1 cascade, 1297x840 bench camera, linear dt0=2^-7 growth 1/256"
+        elif name == "cfg4":
+            t512 = P.GridTransform.cube(512, (-1.0, -1.0, -1.0), 2.0)
+            bits, occ = P.generate_scene("blobs", t512, seed=1)
+            self.objects = [dict(label="blobs s1 512^3", levels=[(t512, bits)], occupancy=occ)]
+            self.schedule = P.StepSchedule.constant(0.5 * t512.voxel_size)
+            self.n_probe = 1 << 24
+            self.desc = "512^3 blobs s1 (1.44%), 2^24 make_probe_rays, dt0 = half voxel"
+        else:
+            raise SystemExit(f"unknown config {name}")
+
+    def rays_per_object(self) -> int:
+        return self.n_probe if self.name == "cfg4" else self.width * self.height
+
+    def fill_rays(self, out, step_index: int, obj: int, rank: int, world: int):
+        """Write the rays of (global step, object) for this rank into the CUDA tensor `out`."""
+        P = self.P
+        if self.name == "cfg4":
+            import torch
+
+            t = self.objects[0]["levels"][0][0]
+            h = P.make_probe_rays(t, self.n_probe, seed=1000 + step_index * world + rank)
+            out.copy_(torch.from_numpy(h))
+            return
+        view = (step_index * world + rank) + obj * (N_VIEWS // max(1, len(self.objects)))
+        if self.name in ("cfg1", "cfg3") and step_index * world + rank == 0:
+            view = 0
+        cam = orbit_camera(P, view, self.width, self.height)
+        cam.rays_device(0, self.width * self.height, out=out)
+
+    def host_rays(self, step_index: int, obj: int, rank: int, world: int) -> np.ndarray:
+        P = self.P
+        if self.name == "cfg4":
+            t = self.objects[0]["levels"][0][0]
+            return P.make_probe_rays(t, self.n_probe, seed=1000 + step_index * world + rank)
+        view = (step_index * world + rank) + obj * (N_VIEWS // max(1, len(self.objects)))
+        if self.name in ("cfg1", "cfg3") and step_index * world + rank == 0:
+            view = 0
+        return orbit_camera(P, view, self.width, self.height).rays()
+
+
+def grid_bytes(P, levels_bits, analyzer):
+    if analyzer == P.Analyzer.dda:
+        return sum(int(b.size) for _, b in levels_bits)
+    return None  # filled from the VDB info
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_10272_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    wl = Workload(P, args.config)
+    n_obj = len(wl.objects)
+    # --- grids: rank 0's payloads broadcast once over NVLink (NCCL), VDB built per rank (K1)
+    grids = []
+    build_ms = []
+    for o in wl.objects:
+        dense_lv, vdb_lv = [], []
+        for t, bits in o["levels"]:
+            d_bits = torch.from_numpy(bits).to(dev)
+            if world > 1:
+                dist.broadcast(d_bits, src=0)
+            dg = P.DenseGrid(t, d_bits)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            vg = P.build_sparse(dg)
+            e1.record()
+            torch.cuda.synchronize()
+            build_ms.append(e0.elapsed_time(e1))
+            dense_lv.append(dg)
+            vdb_lv.append(vg)
+        grids.append((dense_lv, vdb_lv))
+    vdb_bytes = [sum(int(v.memory_bytes()) for v in vl) for _, vl in grids]
+    dense_bytes = [sum(int(t.payload_bytes()) for t, _ in o["levels"]) for o in wl.objects]
+
+    variants = {
+        "hdda_skip": (P.Analyzer.hdda, P.KernelKind.skip),
+        "dda_branch": (P.Analyzer.dda, P.KernelKind.branch),
+        "dda_skip": (P.Analyzer.dda, P.KernelKind.skip),
+    }
+    if args.variants:
+        variants = {k: v for k, v in variants.items() if k in args.variants.split(",")}
+    samplers = {}
+    for vname, (an, kk) in variants.items():
+        samplers[vname] = [P.Sampler(grids[i][1] if an == P.Analyzer.hdda else grids[i][0], an, kk,
+                                     wl.schedule, cascade=wl.cascade) for i in range(n_obj)]
+
+    nr = wl.rays_per_object()
+    steps_total = args.warmup + args.steps
+    # --- rays for every (step, object) in HBM before timing
+    rays = [[torch.empty((nr, 8), dtype=torch.float64, device=dev) for _ in range(n_obj)]
+            for _ in range(steps_total)]
+    for s in range(steps_total):
+        for o in range(n_obj):
+            wl.fill_rays(rays[s][o], s, o, rank, world)
+    torch.cuda.synchronize()
+
+    packed = [torch.empty((nr, 2), dtype=torch.int64, device=dev) for _ in range(n_obj)]
+    stats = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(n_obj)]
+    # --- sizing pass (untimed): totals of every (step, object) -> output capacity per object
+    totals = {}
+    cap = [0] * n_obj
+    for vname, smp in samplers.items():
+        for s in range(steps_total):
+            for o in range(n_obj):
+                smp[o].count(rays[s][o], packed_info=packed[o], stats=stats[o])
+                tot = int(stats[o][0].item())
+                totals[(vname, s, o)] = tot
+                cap[o] = max(cap[o], tot)
+    outs = []
+    for o in range(n_obj):
+        c = max(1, cap[o])
+        outs.append(dict(t_starts=torch.empty(c, dtype=torch.float64, device=dev),
+                         t_ends=torch.empty(c, dtype=torch.float64, device=dev),
+                         ray_indices=torch.empty(c, dtype=torch.int32, device=dev),
+                         cells=torch.empty(c, dtype=torch.int32, device=dev)))
+    # hit rays per (step, object) for the write kernel's algorithmic bytes
+    hits = {}
+    for s in range(steps_total):
+        for o in range(n_obj):
+            smp = samplers[next(iter(samplers))][o]
+            smp.count(rays[s][o], packed_info=packed[o], stats=stats[o])
+            hits[(s, o)] = int((packed[o][:, 1] > 0).sum().item())
+
+    stream = torch.cuda.current_stream()
+    results = {}
+    for vname, smp in samplers.items():
+        def one_step(s, ev=None):
+            for o in range(n_obj):
+                if ev is not None:
+                    ev[o][0].record(stream)
+                smp[o].count(rays[s][o], packed_info=packed[o], stats=stats[o])
+                if ev is not None:
+                    ev[o][1].record(stream)
+                o_ = outs[o]
+                smp[o].write(rays[s][o], packed[o], totals[(vname, s, o)], ray_index_base=0,
+                             out=o_, cells=True, levels=False)
+                if ev is not None:
+                    ev[o][2].record(stream)
+
+        for s in range(args.warmup):
+            one_step(s)
+        evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_obj)]
+               for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            t0.record(stream)
+            for k in range(args.steps):
+                one_step(args.warmup + k, evs[k])
+            t1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = t0.elapsed_time(t1)
+        count_ms = sum(evs[k][o][0].elapsed_time(evs[k][o][1]) for k in range(args.steps) for o in range(n_obj))
+        write_ms = sum(evs[k][o][1].elapsed_time(evs[k][o][2]) for k in range(args.steps) for o in range(n_obj))
+        samples = sum(totals[(vname, args.warmup + k, o)] for k in range(args.steps) for o in range(n_obj))
+        nhit = sum(hits[(args.warmup + k, o)] for k in range(args.steps) for o in range(n_obj))
+        results[vname] = dict(ms=ms, count_ms=count_ms, write_ms=write_ms, samples=samples,
+                              hit_rays=nhit, clocks=clk.summary())
+
+    # --- e2e through the host C-ABI entry point (pinned host buffers, H2D/D2H timed)
+    e2e = None
+    if not args.no_e2e:
+        smp = samplers[next(iter(samplers))]
+        vname0 = next(iter(samplers))
+        h_rays = []
+        for s in range(steps_total):
+            row = []
+            for o in range(n_obj):
+                t = torch.empty((nr, 8), dtype=torch.float64, pin_memory=True)
+                t.copy_(rays[s][o], non_blocking=False)
+                row.append(t)
+            h_rays.append(row)
+        hcap = max(cap)
+        h_out = dict(packed_info=torch.empty((nr, 2), dtype=torch.int64, pin_memory=True).numpy(),
+                     t_starts=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
+                     t_ends=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
+                     ray_indices=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy(),
+                     cells=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
+                     stats=np.zeros(8, np.int64))
+        lib = P.lib
+
+        def e2e_step(s):
+            for o in range(n_obj):
+                rc = lib.sogk_sample_host(smp[o]._h, h_rays[s][o].data_ptr(), nr, 0, hcap,
+                                          h_out["packed_info"].ctypes.data, h_out["t_starts"].ctypes.data,
+                                          h_out["t_ends"].ctypes.data, h_out["ray_indices"].ctypes.data,
+                                          h_out["cells"].ctypes.data, None, None, None,
+                                          h_out["stats"].ctypes.data, stream.cuda_stream or None)
+                P._check(rc, "sample_host")
+
+        for s in range(args.warmup):
+            e2e_step(s)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ts = time.perf_counter()
+        for k in range(args.steps):
+            e2e_step(args.warmup + k)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - ts
+        if world > 1:
+            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        samples0 = sum(totals[(vname0, args.warmup + k, o)] for k in range(args.steps) for o in range(n_obj))
+        e2e = dict(seconds=e2e_s, h2d=nr * 64 * n_obj, d2h_per_run=samples0 * 24 / args.steps + nr * 16 * n_obj)
+
+    # --- max over ranks
+    def rmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def rsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    agg = {}
+    for vname, r in results.items():
+        agg[vname] = dict(ms=rmax(r["ms"]), samples=rsum(r["samples"]), count_ms=r["count_ms"],
+                          write_ms=r["write_ms"], hit_rays=r["hit_rays"], local_samples=r["samples"],
+                          clocks=r["clocks"])
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    head = "hdda_skip" if "hdda_skip" in agg else next(iter(agg))
+    h = agg[head]
+    total_rays = nr * n_obj * args.steps * world
+    sec = h["ms"] / 1e3
+    rays_s = total_rays / sec
+    samples_s = h["samples"] / sec
+    peak, peak_src = load_peaks()
+    # roofline: dominant kernel (larger share of the step) with its algorithmic bytes
+    launches = args.steps * n_obj
+    nr_loc = nr * n_obj * args.steps
+    write_bytes = nr_loc * 16 + h["hit_rays"] * 64 + h["local_samples"] * 24
+    count_bytes = nr_loc * (64 + 16)
+    if h["write_ms"] >= h["count_ms"]:
+        dom, dom_ms, dom_bytes = "write_kernel (pass 2)", h["write_ms"], write_bytes
+    else:
+        dom, dom_ms, dom_bytes = "count_kernel (pass 1 + fused scan)", h["count_ms"], count_bytes
+    achieved = dom_bytes / launches / (dom_ms / launches / 1e3) / 1e9
+    step_bytes = nr_loc * (64 + 16) + h["local_samples"] * 24 + sum(vdb_bytes) * args.steps
+    step_gbs = step_bytes / (h["ms"] / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "rays/sec and samples/sec per B200 (and 8-GPU box), HDDA-VDB vs dense-DDA, % HBM roofline",
+        "value": rays_s,
+        "unit": "rays/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": h["ms"] / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (procedural occupancy grids from the reference generators, camera/probe rays)",
+        "config": {"workload": args.config, "desc": wl.desc, "variant": "sparse+hdda+skip" if head == "hdda_skip" else head,
+                   "rays_per_step": nr * n_obj * world, "objects": [o["label"] for o in wl.objects],
+                   "parallelism": f"rays sharded by view over {world} GPU(s)",
+                   "l2": "inputs+outputs per step > 126 MB L2 (no flush)"},
+        "samples_per_sec": samples_s,
+        "samples_per_step": h["samples"] / args.steps,
+        "variants": {k: {"rays_per_sec": total_rays / (v["ms"] / 1e3),
+                         "samples_per_sec": v["samples"] / (v["ms"] / 1e3),
+                         "ms_per_step": v["ms"] / args.steps,
+                         "count_ms_per_step": v["count_ms"] / args.steps,
+                         "write_ms_per_step": v["write_ms"] / args.steps} for k, v in agg.items()},
+        "hdda_vs_dda_branch": (agg["dda_branch"]["ms"] / agg["hdda_skip"]["ms"]) if {"dda_branch", "hdda_skip"} <= agg.keys() else None,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": dom_bytes / launches},
+        "step_roofline": {"bytes_per_step": step_bytes / args.steps, "achieved_gbs": step_gbs,
+                          "frac": step_gbs / peak,
+                          "basis": "N_rays*(64+16) + N_samples*24 + VDB bytes (SURVEY §8d)"},
+        "vdb_build_ms": build_ms,
+        "grid_bytes": {"dense": dense_bytes, "vdb_sog1": vdb_bytes},
+        "gpu_launches": 2 * launches,
+        "clocks": h["clocks"],
+    }
+    if e2e:
+        line["e2e"] = {"value": total_rays / e2e["seconds"], "unit": "rays/s",
+                       "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["d2h_per_run"]),
+                       "api": "sogk_sample_host (pinned host rays in, packed host samples out)"}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(P, wl, args)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the unmodified reference headers) — baseline only
+# ---------------------------------------------------------------------------
+def _ref_sampler(wl, analyzer, kernel):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import Grid, RefLib
+
+    R = RefLib()
+    out = []
+    for o in wl.objects:
+        lv = [Grid(t.resolution, t.world_min, t.voxel_size, b) for t, b in o["levels"]]
+        out.append(R.sampler(lv, analyzer, kernel, wl.schedule.kind, wl.schedule.dt0,
+                             wl.schedule.growth, cascade=wl.cascade))
+    return R, out
+
+
+def _cpu_sample(wl, stride, step_index, rank=0, world=1):
+    return [wl.host_rays(step_index, o, rank, world)[::stride].copy() for o in range(len(wl.objects))]
+
+
+def _spin_mask(wl, rays_per_obj):
+    """Rays on which the reference HDDA never returns are screened out with the
+    capped oracle detector; they are excluded from the CPU timing and counted."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import HDDA, SKIP, Grid, Oracle
+
+    O = Oracle()
+    masks = []
+    for o, r in zip(wl.objects, rays_per_obj):
+        lv = [Grid(t.resolution, t.world_min, t.voxel_size, b) for t, b in o["levels"]]
+        s = O.sampler(lv, HDDA, SKIP, wl.schedule.kind, wl.schedule.dt0, wl.schedule.growth,
+                      cascade=wl.cascade)
+        masks.append((O.sample(s, r).status == 2).astype(np.uint8))
+    return masks
+
+
+def cpu_baseline(P, wl, args):
+    from oracle_bindings import HDDA, SKIP
+
+    try:
+        R, smp = _ref_sampler(wl, HDDA, SKIP)
+    except FileNotFoundError:
+        return {"value": None, "unit": "rays/s", "kind": "reference", "cores": 0,
+                "sample": "oracle/_ref missing"}
+    cores = os.cpu_count() or 1
+    stride = args.cpu_stride
+    rays = _cpu_sample(wl, stride, 0)
+    masks = _spin_mask(wl, rays)
+    sec, n = 0.0, 0
+    for s, r, m in zip(smp, rays, masks):
+        dt, _ = s.time(r, skip=m, threads=cores, reps=1)
+        sec += dt
+        n += int(r.shape[0] - m.sum())
+    return {"value": n / sec, "unit": "rays/s", "cores": cores, "kind": "reference",
+            "sample": f"sparse+hdda+skip via sog::run_sampler, every {stride}th ray of step 0 "
+                      f"({n} rays over {len(rays)} object(s)), {cores} threads, spin-screened "
+                      f"{int(sum(m.sum() for m in masks))} rays"}
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU sampler (oracle/_ref) on the host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2404_10272_b200 as P
+    from oracle_bindings import HDDA, SKIP
+
+    wl = Workload(P, args.config)
+    try:
+        R, smp = _ref_sampler(wl, HDDA, SKIP)
+    except FileNotFoundError as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
+        return
+    cores = os.cpu_count() or 1
+    stride = args.cpu_stride
+    step_rays, step_masks = [], []
+    for s in range(args.warmup + args.steps):
+        r = _cpu_sample(wl, stride, s, 0, 1)
+        step_rays.append(r)
+        step_masks.append(_spin_mask(wl, r))
+    per_step_rays = [sum(int(x.shape[0] - m.sum()) for x, m in zip(r, mm)) for r, mm in zip(step_rays, step_masks)]
+
+    def step(s):
+        t = 0.0
+        for sm, r, m in zip(smp, step_rays[s], step_masks[s]):
+            dt, _ = sm.time(r, skip=m, threads=cores, reps=1)
+            t += dt
+        return t
+
+    for s in range(args.warmup):
+        step(s)
+    total_s = 0.0
+    n = 0
+    for k in range(args.steps):
+        total_s += step(args.warmup + k)
+        n += per_step_rays[args.warmup + k]
+    v = n / total_s
+    line = {
+        "impl": "reference",
+        "metric": "rays/sec and samples/sec per B200 (and 8-GPU box), HDDA-VDB vs dense-DDA, % HBM roofline",
+        "value": v, "unit": "rays/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_s / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": wl.desc, "variant": "sparse+hdda+skip"},
+        "cpu_baseline": {"value": v, "unit": "rays/s", "cores": cores, "kind": "reference",
+                         "sample": f"every {stride}th ray of each step's views, sog::run_sampler on {cores} threads"},
+        "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--variants", default="")
+    ap.add_argument("--cpu-stride", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -486,6 +486,8 @@ class Sampler:
         ri = o.get("ray_indices", torch.empty(total, dtype=torch.int32, device=dev))
         ce = o.get("cells", torch.empty(total, dtype=torch.int32, device=dev)) if cells else None
         lv = o.get("levels", torch.empty(total, dtype=torch.uint8, device=dev)) if levels else None
+        if total == 0:  # nothing to write (empty tensors have no device address)
+            return ts, te, ri, ce, lv
         _check(lib.sogk_sample_write(self._h, _ptr(rays), rays.shape[0], _ptr(packed_info),
                                      ray_index_base, _ptr(ts), _ptr(te), _ptr(ri), _ptr(ce),
                                      _ptr(lv), _stream(stream)), "sample_write")
