@@ -4,8 +4,10 @@
 
 #include <algorithm>
 #include <array>
+#include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -117,6 +119,13 @@ struct sogk_grid {
             g.R[a] = R[a];
         }
         g.voxel = t.voxel_size;
+        g.inv_voxel = 1.0 / t.voxel_size;
+        {
+            int e = 0;
+            const double m = std::frexp(t.voxel_size, &e);
+            // exact reciprocal and no subnormal products for grid-scale values
+            g.voxel_pow2 = (m == 0.5 && e > -900 && e < 900) ? 1 : 0;
+        }
         const double h = t.voxel_size * 0.5; // center_bounds, sampling.hpp:248-251
         for (int a = 0; a < 3; ++a) {
             g.clo[a] = t.world_min[a] + h;
@@ -164,17 +173,31 @@ struct sogk_sampler {
         cudaFree(hb);
     }
 
+    // pass 1 -> pass 2 handshake: the resume states of the last count call
+    const void* last_rays = nullptr;
+    int64_t last_first = -1, last_n = -1;
+    bool last_cam = false;
+    bool persistent = false; // SOGK_PERSISTENT=1 selects the persistent-thread kernels (slower here)
+
+    // workspace = [scan tile states | tile counter | resume states]
     int ensure_ws(int64_t n) {
-        const int64_t blocks = (n + 255) / 256;
-        const size_t need = size_t(blocks) * 8 + 16;
+        const size_t need = scan_off(n) + resume_bytes(n);
         if (need <= ws_bytes) return SOGK_OK;
         cudaFree(ws);
         ws = nullptr;
         ws_bytes = 0;
+        last_n = -1;
         CK(cudaMalloc(&ws, need), "sampler workspace");
         ws_bytes = need;
         return SOGK_OK;
     }
+    static size_t scan_off(int64_t n) { return ((size_t(scan_tiles(n)) * 8 + 64 + 255) / 256) * 256; }
+    // [tiles | scan ctr (8B) | count ray ctr (8B) | write ray ctr (8B)]
+    unsigned long long* ray_ctr(int64_t n, int which) const {
+        return reinterpret_cast<unsigned long long*>(tiles() + scan_tiles(n) + 1 + which);
+    }
+    uint64_t* tiles() const { return static_cast<uint64_t*>(ws); }
+    void* resume(int64_t n) const { return static_cast<char*>(ws) + scan_off(n); }
 };
 
 // ---------------------------------------------------------------------------
@@ -745,11 +768,24 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     s->v.cascade = cascade ? 1 : 0;
     s->v.branch = desc->kernel == SOGK_BRANCH ? 1 : 0;
     s->v.linear = desc->schedule == SOGK_LINEAR ? 1 : 0;
+    if (const char* e = std::getenv("SOGK_PERSISTENT")) s->persistent = std::atoi(e) != 0;
+    s->dev.refill_min = 1;
+    if (const char* e = std::getenv("SOGK_REFILL")) s->dev.refill_min = std::max(1, std::min(32, std::atoi(e)));
     for (int b = 0; b < n_levels; ++b) s->dev.lv[b] = levels[b]->dev();
     s->dev.n_levels = n_levels;
     s->dev.spin_cap = desc->spin_cap > 0 ? desc->spin_cap : SOGK_DEFAULT_SPIN_CAP;
     s->dev.dt0 = desc->dt0;
+    s->dev.inv_dt0 = 1.0 / desc->dt0;
     s->dev.growth = desc->schedule == SOGK_LINEAR ? desc->growth : 0.0;
+    // largest t with fl(growth * t) <= dt0: below it the linear step is the constant dt0
+    if (s->dev.growth > 0.0) {
+        double x = desc->dt0 / s->dev.growth;
+        while (s->dev.growth * x > desc->dt0) x = std::nextafter(x, 0.0);
+        while (s->dev.growth * std::nextafter(x, DBL_MAX) <= desc->dt0) x = std::nextafter(x, DBL_MAX);
+        s->dev.t_switch = x;
+    } else {
+        s->dev.t_switch = DBL_MAX;
+    }
     *out = s;
     return SOGK_OK;
 }
@@ -787,15 +823,21 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     if (n == 0) return SOGK_OK;
     int st = s->ensure_ws(n);
     if (st) return st;
-    const int64_t blocks = (n + 255) / 256;
-    CK(cudaMemsetAsync(s->ws, 0, size_t(blocks) * 8 + 16, S(stream)), "workspace reset");
-    uint64_t* tiles = static_cast<uint64_t*>(s->ws);
-    unsigned int* ctr = reinterpret_cast<unsigned int*>(tiles + blocks);
+    const int64_t tiles = scan_tiles(n);
+    CK(cudaMemsetAsync(s->ws, 0, size_t(tiles) * 8 + 64, S(stream)), "workspace reset");
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
+    void* resume = s->resume(n);
     CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
-                    d_status, d_counters, tiles, ctr, S(stream)),
+                    d_status, d_counters, resume, s->persistent ? s->ray_ctr(n, 0) : nullptr, S(stream)),
        "count launch");
+    CK(launch_scan(n, d_packed, d_stats, s->tiles(),
+                   reinterpret_cast<unsigned int*>(s->tiles() + tiles), S(stream)),
+       "scan launch");
+    s->last_rays = cam ? nullptr : d_rays;
+    s->last_cam = cam != nullptr;
+    s->last_first = first;
+    s->last_n = n;
     return SOGK_OK;
 }
 
@@ -827,8 +869,19 @@ static int write_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     if (!d_packed || !ts || (!cam && !d_rays)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
-    CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, base, ts, te,
-                    ri, ce, lv, S(stream)),
+    // resume states are valid when pass 1 ran on this sampler with the same rays
+    const bool same = s->last_n == n && s->last_cam == (cam != nullptr) &&
+                      (cam ? s->last_first == first : s->last_rays == d_rays);
+    const void* resume = same ? s->resume(n) : nullptr;
+    unsigned long long* ctr = nullptr;
+    if (s->persistent) {
+        int st = s->ensure_ws(n);
+        if (st) return st;
+        ctr = s->ray_ctr(n, 1);
+        CK(cudaMemsetAsync(ctr, 0, 8, S(stream)), "write counter reset");
+    }
+    CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, resume, base,
+                    ts, te, ri, ce, lv, ctr, S(stream)),
        "write launch");
     return SOGK_OK;
 }

@@ -11,6 +11,7 @@
 #include <cfloat>
 #include <cstdint>
 
+#include "sogk_ladder.cuh"
 #include "sogk_layout.h"
 
 namespace sogk {
@@ -97,8 +98,10 @@ struct Geom {
         t_enter = te;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            dir[a] = r.d[a] / g.voxel;
-            entry[a] = (r.o[a] + r.d[a] * te - g.wmin[a]) / g.voxel;
+            // x / voxel; for a power-of-two voxel this equals x * (1/voxel) exactly
+            dir[a] = g.voxel_pow2 ? r.d[a] * g.inv_voxel : r.d[a] / g.voxel;
+            const double num = r.o[a] + r.d[a] * te - g.wmin[a];
+            entry[a] = g.voxel_pow2 ? num * g.inv_voxel : num / g.voxel;
             if (dir[a] > 0.0) {
                 step[a] = 1;
                 inv[a] = 1.0 / dir[a];
@@ -147,17 +150,6 @@ struct Geom {
     }
 };
 
-__device__ __forceinline__ int argmin_axis(double t0, double t1, double t2) { // :107-112
-    int axis = 0;
-    double m = t0;
-    if (t1 < m) {
-        axis = 1;
-        m = t1;
-    }
-    if (t2 < m) axis = 2;
-    return axis;
-}
-
 struct Event {
     int ijk[3];
     int level;
@@ -167,8 +159,8 @@ struct Event {
 };
 
 __device__ __forceinline__ bool in_bounds(const GridDev& g, const int ijk[3]) {
-    return ijk[0] >= 0 && ijk[1] >= 0 && ijk[2] >= 0 && ijk[0] < g.res[0] && ijk[1] < g.res[1] &&
-           ijk[2] < g.res[2];
+    return (unsigned)ijk[0] < (unsigned)g.res[0] && (unsigned)ijk[1] < (unsigned)g.res[1] &&
+           (unsigned)ijk[2] < (unsigned)g.res[2];
 }
 
 // DenseGrid::voxel_at, grid.hpp:129-133
@@ -192,19 +184,21 @@ struct Query {
     bool occ;
 };
 
-struct VdbCursor {
-    int leaf_origin[3];
-    int64_t leaf; // cached leaf index, -1 = none
+constexpr int kNoLeaf = -(1 << 29); // leaf-cache origin that no coordinate can hit
 
-    __device__ __forceinline__ void reset() { leaf = -1; }
+struct VdbCursor {
+    int lo[3];       // cached leaf origin (kNoLeaf: none)
+    int64_t leaf;    // cached leaf index
+
+    __device__ __forceinline__ void reset() { lo[0] = lo[1] = lo[2] = kNoLeaf; leaf = 0; }
 
     __device__ __forceinline__ Query query(const GridDev& g, const int ijk[3]) {
         Query q;
-        if (leaf >= 0 && ijk[0] >= leaf_origin[0] && ijk[1] >= leaf_origin[1] &&
-            ijk[2] >= leaf_origin[2] && ijk[0] < leaf_origin[0] + 8 &&
-            ijk[1] < leaf_origin[1] + 8 && ijk[2] < leaf_origin[2] + 8) {
-            const uint64_t w = __ldg(g.leaves + leaf * 8 + (ijk[2] & 7));
-            q.occ = (w >> (((ijk[1] & 7) << 3) | (ijk[0] & 7))) & 1ull;
+        const unsigned lx = (unsigned)(ijk[0] - lo[0]), ly = (unsigned)(ijk[1] - lo[1]),
+                       lz = (unsigned)(ijk[2] - lo[2]);
+        if ((lx | ly | lz) < 8u) { // cached leaf hit (Accessor fast path, sparse.hpp:229-233)
+            const uint64_t w = __ldg(g.leaves + leaf * 8 + lz);
+            q.occ = (w >> ((ly << 3) | lx)) & 1ull;
             q.level = LV_VOXEL;
             q.extent = 1;
             q.origin[0] = ijk[0];
@@ -212,45 +206,37 @@ struct VdbCursor {
             q.origin[2] = ijk[2];
             return q;
         }
-        if (!in_bounds(g, ijk)) { // background root tile of the 128-aligned region
-            q.occ = false;
-            q.level = LV_ROOT_TILE;
-            q.extent = 128;
-            q.origin[0] = (ijk[0] >> 7) << 7; // floor_div (vec.hpp:68-76) * 128
-            q.origin[1] = (ijk[1] >> 7) << 7;
-            q.origin[2] = (ijk[2] >> 7) << 7;
-            return q;
-        }
-        const int rx = ijk[0] >> 7, ry = ijk[1] >> 7, rz = ijk[2] >> 7;
-        const int region = (rz * g.R[1] + ry) * g.R[0] + rx;
+        q.occ = false;
+        q.level = LV_ROOT_TILE;
+        q.extent = 128;
+        q.origin[0] = (ijk[0] >> 7) << 7; // region_origin = floor_div(ijk, 128) * 128 (:159)
+        q.origin[1] = (ijk[1] >> 7) << 7;
+        q.origin[2] = (ijk[2] >> 7) << 7;
+        if (!in_bounds(g, ijk)) return q; // background root tile (:164-165)
+        const int region = ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7);
         const int32_t node = __ldg(g.root + region);
-        if (node < 0) { // root tile (collapsed region)
+        q.level = LV_INTERNAL_TILE;
+        if (node < 0) { // collapsed region (root tile)
             q.occ = node == kRootOccupied;
-            q.level = LV_INTERNAL_TILE;
-            q.extent = 128;
-            q.origin[0] = rx << 7;
-            q.origin[1] = ry << 7;
-            q.origin[2] = rz << 7;
             return q;
         }
-        const int cx = (ijk[0] >> 3) & 15, cy = (ijk[1] >> 3) & 15, cz = (ijk[2] >> 3) & 15;
-        const int ci = (cz * 16 + cy) * 16 + cx;
+        const int ci = ((((ijk[2] >> 3) & 15) * 16 + ((ijk[1] >> 3) & 15)) * 16) + ((ijk[0] >> 3) & 15);
         const int64_t wi = (int64_t)node * 64 + (ci >> 6);
         const uint64_t cm = __ldg(g.child_mask + wi);
         const int b = ci & 63;
-        if (!((cm >> b) & 1ull)) { // tile child
+        q.origin[0] = ijk[0] & ~7;
+        q.origin[1] = ijk[1] & ~7;
+        q.origin[2] = ijk[2] & ~7;
+        if (!((cm >> b) & 1ull)) { // tile child (:205-208)
             q.occ = (__ldg(g.value_mask + wi) >> b) & 1ull;
             q.level = LV_LEAF_TILE;
             q.extent = 8;
-            q.origin[0] = ijk[0] & ~7;
-            q.origin[1] = ijk[1] & ~7;
-            q.origin[2] = ijk[2] & ~7;
             return q;
         }
         leaf = (int64_t)__ldg(g.prefix + wi) + __popcll(cm & ((1ull << b) - 1ull));
-        leaf_origin[0] = ijk[0] & ~7;
-        leaf_origin[1] = ijk[1] & ~7;
-        leaf_origin[2] = ijk[2] & ~7;
+        lo[0] = q.origin[0];
+        lo[1] = q.origin[1];
+        lo[2] = q.origin[2];
         const uint64_t w = __ldg(g.leaves + leaf * 8 + (ijk[2] & 7));
         q.occ = (w >> (((ijk[1] & 7) << 3) | (ijk[0] & 7))) & 1ull;
         q.level = LV_VOXEL;
@@ -261,6 +247,22 @@ struct VdbCursor {
         return q;
     }
 };
+
+// argmin with ties toward the lowest axis (argmin_axis, traversal.hpp:107-112),
+// written as compare-and-select so that no branch is emitted
+__device__ __forceinline__ int argmin3(double a, double b, double c, double& m) {
+    int axis = 0;
+    m = a;
+    if (b < m) {
+        m = b;
+        axis = 1;
+    }
+    if (c < m) {
+        m = c;
+        axis = 2;
+    }
+    return axis;
+}
 
 // ---------------------------------------------------------------------------
 // Analyzers.  next() returns 1 with an event, 0 at end of stream, and sets
@@ -273,9 +275,18 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
     int np[3];
     double tn[3];
     double t_cur;
+    int64_t lin;        // linear voxel index of ijk (x-fastest), kept incrementally
+    int64_t stride[3];  // signed linear-index step per axis
     int lookups, steps;
     bool done;
     bool undefined;
+
+    __device__ __forceinline__ void set_lin(const GridDev& g) {
+        lin = ((int64_t)ijk[2] * g.res[1] + ijk[1]) * g.res[0] + ijk[0];
+        stride[0] = geom.step[0];
+        stride[1] = (int64_t)geom.step[1] * g.res[0];
+        stride[2] = (int64_t)geom.step[2] * g.res[0] * g.res[1];
+    }
 
     __device__ __forceinline__ void init(const Ray& r, const GridDev& g, int /*spin_cap*/) {
         lookups = steps = 0;
@@ -287,16 +298,14 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
         t_cur = geom.t_enter;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            if (geom.step[a] == 0) {
-                np[a] = 0;
-                tn[a] = kInf;
-            } else {
-                np[a] = ijk[a] + (geom.step[a] > 0 ? 1 : 0);
-                tn[a] = geom.plane_t(a, (double)np[a]);
-            }
+            np[a] = ijk[a] + (geom.step[a] > 0 ? 1 : 0);
+            tn[a] = geom.step[a] == 0 ? kInf : geom.plane_t(a, (double)np[a]);
         }
+        set_lin(g);
     }
 
+    // ijk is always inside the grid while the stream is live (entry_cell clamps,
+    // advance() ends the stream on leaving), so the lookup needs no bounds test
     __device__ __forceinline__ void emit(const GridDev& g, double t1, Event& ev) { // :171-175
         ++steps;
         ++lookups;
@@ -306,45 +315,59 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
         ev.level = LV_VOXEL;
         ev.t0 = t_cur;
         ev.t1 = t1;
-        ev.occ = dense_voxel(g, ijk);
+        ev.occ = (__ldg(g.bits + (lin >> 3)) >> (lin & 7)) & 1u;
     }
 
     __device__ __forceinline__ void advance(const GridDev& g, int axis) { // :177-182
-        // select-based updates keep the per-axis arrays in registers
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            if (a != axis) continue;
-            ijk[a] += geom.step[a];
-            np[a] += geom.step[a];
-            tn[a] = geom.plane_t(a, (double)np[a]);
-            if (ijk[a] < 0 || ijk[a] >= g.res[a]) done = true;
+            if (a == axis) {
+                ijk[a] += geom.step[a];
+                np[a] += geom.step[a];
+                tn[a] = geom.plane_t(a, (double)np[a]);
+                lin += stride[a];
+                if ((unsigned)ijk[a] >= (unsigned)g.res[a]) done = true;
+            }
         }
     }
 
-    __device__ __forceinline__ int next(const GridDev& g, Event& ev) { // :143-162
+    // One iteration of DdaTraversal::next's loop (:143-162): 1 = event, 0 = end of
+    // stream, -1 = degenerate corner crossing consumed (call again).  Callers
+    // loop; keeping the retry out of here keeps kernels to one flat loop.
+    __device__ __forceinline__ int next(const GridDev& g, Event& ev) {
         if (done) return 0;
-        for (;;) {
-            const int axis = argmin_axis(tn[0], tn[1], tn[2]);
-            const double t1 = axis == 0 ? tn[0] : (axis == 1 ? tn[1] : tn[2]);
-            if (t1 >= geom.t_exit) {
-                done = true;
-                emit(g, geom.t_exit, ev);
-                return 1;
-            }
-            if (t1 <= t_cur) { // degenerate corner crossing, advance silently
-                advance(g, axis);
-                if (done) return 0;
-                continue;
-            }
-            emit(g, t1, ev);
-            t_cur = t1;
-            advance(g, axis);
+        double t1;
+        const int axis = argmin3(tn[0], tn[1], tn[2], t1);
+        if (t1 >= geom.t_exit) {
+            done = true;
+            emit(g, geom.t_exit, ev);
             return 1;
         }
+        if (t1 <= t_cur) { // degenerate corner crossing, advance silently
+            advance(g, axis);
+            return done ? 0 : -1;
+        }
+        emit(g, t1, ev);
+        t_cur = t1;
+        advance(g, axis);
+        return 1;
     }
 
     __device__ __forceinline__ bool probe(const GridDev& g, const Event& ev) const { // DenseProbe
         return dense_voxel(g, ev.ijk);
+    }
+
+    // Resume at an emitted event: (ijk, t_cur) = (ev.ijk, ev.t0) reproduces it.
+    __device__ __forceinline__ void restore(const GridDev& g, const int in_ijk[3], double in_t) {
+        done = false;
+        t_cur = in_t;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            ijk[a] = in_ijk[a];
+            np[a] = ijk[a] + (geom.step[a] > 0 ? 1 : 0);
+            tn[a] = geom.step[a] == 0 ? kInf : geom.plane_t(a, (double)np[a]);
+        }
+        set_lin(g);
     }
 };
 
@@ -355,6 +378,7 @@ struct HddaAn { // HddaTraversal, traversal.hpp:199-264
     double t_cur;
     int lookups, steps;
     int spin_cap;
+    int degenerate; // consecutive degenerate iterations
     bool done;
     bool undefined;
     VdbCursor cur;
@@ -363,6 +387,7 @@ struct HddaAn { // HddaTraversal, traversal.hpp:199-264
         lookups = steps = 0;
         undefined = false;
         spin_cap = cap;
+        degenerate = 0;
         cur.reset();
         geom.init(r, g);
         done = !geom.valid;
@@ -371,25 +396,27 @@ struct HddaAn { // HddaTraversal, traversal.hpp:199-264
         t_cur = geom.t_enter;
     }
 
-    __device__ __forceinline__ int next(const GridDev& g, Event& ev) { // :213-248
+    // One iteration of HddaTraversal::next's loop (:213-248): 1 = event, 0 = end,
+    // -1 = degenerate iteration consumed (call again).
+    __device__ __forceinline__ int next(const GridDev& g, Event& ev) {
         if (done) return 0;
-        int degenerate = 0;
-        for (;;) {
+        {
             const Query q = cur.query(g, ijk);
             ++lookups;
+            // exit plane of the node on each moving axis (:218-228), and the cell
+            // just past it (`stepped`, :236-237)
             double tc[3];
+            int stepped[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                if (geom.step[a] == 0) {
-                    tc[a] = kInf;
-                } else {
-                    const double plane = geom.step[a] > 0 ? (double)(q.origin[a] + q.extent)
-                                                          : (double)q.origin[a];
-                    tc[a] = geom.plane_t(a, plane);
-                }
+                const int hi = q.origin[a] + q.extent;
+                const int plane = geom.step[a] > 0 ? hi : q.origin[a];
+                stepped[a] = geom.step[a] > 0 ? hi : q.origin[a] - 1;
+                const double pt = geom.plane_t(a, (double)plane);
+                tc[a] = geom.step[a] == 0 ? kInf : pt;
             }
-            const int axis = argmin_axis(tc[0], tc[1], tc[2]);
-            const double t1 = axis == 0 ? tc[0] : (axis == 1 ? tc[1] : tc[2]);
+            double t1;
+            const int axis = argmin3(tc[0], tc[1], tc[2], t1);
             ev.ijk[0] = q.origin[0];
             ev.ijk[1] = q.origin[1];
             ev.ijk[2] = q.origin[2];
@@ -402,23 +429,32 @@ struct HddaAn { // HddaTraversal, traversal.hpp:199-264
                 ev.t1 = geom.t_exit;
                 return 1;
             }
-            const int o_ax = axis == 0 ? q.origin[0] : (axis == 1 ? q.origin[1] : q.origin[2]);
-            const int s_ax = axis == 0 ? geom.step[0] : (axis == 1 ? geom.step[1] : geom.step[2]);
-            const int stepped = s_ax > 0 ? o_ax + q.extent : o_ax - 1;
-            if (t1 <= t_cur) { // degenerate corner crossing (:238-241)
-                geom.cell_after_crossing(t_cur, axis, stepped, ijk);
+            const bool degen = t1 <= t_cur; // degenerate corner crossing (:238-241)
+            // cell_after_crossing (:91-104) at t_cur (degenerate) or t1, all axes
+            // evaluated and the stepped one overridden: no data-dependent branch
+            const double tt = degen ? t_cur : t1;
+            const double dt = tt - geom.t_enter;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double gc = geom.entry[a] + dt * geom.dir[a];
+                double c = floor(gc);
+                if (geom.step[a] < 0 && c == gc) c -= 1.0;
+                const int moved = geom.step[a] != 0 ? (int)c : ijk[a];
+                ijk[a] = (a == axis) ? stepped[a] : moved;
+            }
+            if (degen) {
                 // the reference spins forever at exact edge crossings
                 if (++degenerate > spin_cap) {
                     undefined = true;
                     done = true;
                     return 0;
                 }
-                continue;
+                return -1;
             }
+            degenerate = 0;
             ev.t0 = t_cur;
             ev.t1 = t1;
             ++steps;
-            geom.cell_after_crossing(t1, axis, stepped, ijk);
             t_cur = t1;
             return 1;
         }
@@ -426,6 +462,18 @@ struct HddaAn { // HddaTraversal, traversal.hpp:199-264
 
     __device__ __forceinline__ bool probe(const GridDev& g, const Event& ev) { // SparseProbe
         return cur.query(g, ev.ijk).occ;
+    }
+
+    // Resume at an emitted event: the node origin queries the same node, so
+    // (ijk, t_cur) = (ev.ijk, ev.t0) reproduces it.
+    __device__ __forceinline__ void restore(const GridDev&, const int in_ijk[3], double in_t) {
+        done = false;
+        degenerate = 0;
+        t_cur = in_t;
+        ijk[0] = in_ijk[0];
+        ijk[1] = in_ijk[1];
+        ijk[2] = in_ijk[2];
+        cur.reset(); // the accessor cache is semantically transparent
     }
 };
 
@@ -480,7 +528,7 @@ struct CascadeAn {
         int m = 0; // std::unique
         for (int i = 0; i < nc; ++i)
             if (m == 0 || !(cuts[m - 1] == cuts[i])) cuts[m++] = cuts[i];
-        // segments: [cut[k], cut[k+1]) for the kept k; store pairs explicitly
+        // after unique the cuts are strictly increasing, so every pair is a segment
         for (int i = 0; i + 1 < m; ++i) {
             if (!(cuts[i] < cuts[i + 1])) continue;
             const double mid = 0.5 * (cuts[i] + cuts[i + 1]);
@@ -491,7 +539,7 @@ struct CascadeAn {
                     break;
                 }
             cut[n_seg] = cuts[i];
-            cut[n_seg + 1] = cuts[i + 1]; // consecutive kept segments share this boundary
+            cut[n_seg + 1] = cuts[i + 1];
             seg_level[n_seg] = (signed char)level;
             ++n_seg;
         }
@@ -500,42 +548,58 @@ struct CascadeAn {
         t_exit = tx;
     }
 
-    __device__ __forceinline__ int next(const SamplerDev& s, Event& ev) { // :361-392
-        for (;;) {
-            if (has_sub) {
-                const int gl = seg_level[seg];
-                if (sub.next(s.lv[gl], ev)) {
-                    ev.grid_level = gl;
-                    return 1;
-                }
-                if (sub.undefined) {
-                    undefined = true;
-                    return 0;
-                }
-                fin_lookups += sub.lookups;
-                fin_steps += sub.steps;
-                has_sub = false;
-                ++seg;
-            }
-            if (seg >= n_seg) return 0;
+    __device__ __forceinline__ void open_sub(const SamplerDev& s) {
+        Ray sr = ray; // Ray(origin, dir, seg.t0, seg.t1) (:389-390)
+        sr.tmin = cut[seg];
+        sr.tmax = cut[seg + 1];
+        sub.init(sr, s.lv[seg_level[seg]], s.spin_cap);
+        has_sub = true;
+    }
+
+    // One action of CascadeTraversal::next (:361-392): 1 = event, 0 = end,
+    // -1 = internal transition (sub-analyzer step, segment change) — call again.
+    __device__ __forceinline__ int next(const SamplerDev& s, Event& ev) {
+        if (has_sub) {
             const int gl = seg_level[seg];
-            if (gl < 0) { // outside every level: one empty event
-                ev.ijk[0] = ev.ijk[1] = ev.ijk[2] = 0;
-                ev.level = LV_ROOT_TILE;
-                ev.t0 = cut[seg];
-                ev.t1 = cut[seg + 1];
-                ev.occ = false;
-                ev.grid_level = -1;
-                ++seg;
-                ++fin_steps;
-                return 1;
+            const int r = sub.next(s.lv[gl], ev);
+            if (r != 0) {
+                ev.grid_level = gl;
+                return r;
             }
-            Ray sr = ray;
-            sr.tmin = cut[seg];
-            sr.tmax = cut[seg + 1];
-            sub.init(sr, s.lv[gl], s.spin_cap);
-            has_sub = true;
+            if (sub.undefined) {
+                undefined = true;
+                return 0;
+            }
+            fin_lookups += sub.lookups;
+            fin_steps += sub.steps;
+            has_sub = false;
+            ++seg;
+            return -1;
         }
+        if (seg >= n_seg) return 0;
+        const int gl = seg_level[seg];
+        if (gl < 0) { // outside every level: one empty event
+            ev.ijk[0] = ev.ijk[1] = ev.ijk[2] = 0;
+            ev.level = LV_ROOT_TILE;
+            ev.t0 = cut[seg];
+            ev.t1 = cut[seg + 1];
+            ev.occ = false;
+            ev.grid_level = -1;
+            ++seg;
+            ++fin_steps;
+            return 1;
+        }
+        open_sub(s);
+        return -1;
+    }
+
+    // resume inside the sub-analyzer of the current segment
+    __device__ __forceinline__ int resume_tag() const { return seg; }
+    __device__ __forceinline__ void restore(const SamplerDev& s, int tag, const int in_ijk[3],
+                                            double in_t) {
+        seg = tag;
+        open_sub(s);
+        sub.restore(s.lv[seg_level[seg]], in_ijk, in_t);
     }
 
     __device__ __forceinline__ int lookup_count() const {
@@ -581,6 +645,10 @@ struct AnyAn<Sub, false> {
     __device__ __forceinline__ bool probe(const SamplerDev& s, const Event& ev) {
         return an.probe(s.lv[0], ev);
     }
+    __device__ __forceinline__ int resume_tag() const { return 0; }
+    __device__ __forceinline__ void restore(const SamplerDev& s, int, const int ijk[3], double t) {
+        an.restore(s.lv[0], ijk, t);
+    }
 };
 
 template <class Sub>
@@ -597,47 +665,122 @@ struct AnyAn<Sub, true> {
     __device__ __forceinline__ bool probe(const SamplerDev& s, const Event& ev) {
         return an.probe(s, ev);
     }
+    __device__ __forceinline__ int resume_tag() const { return an.resume_tag(); }
+    __device__ __forceinline__ void restore(const SamplerDev& s, int tag, const int ijk[3], double t) {
+        an.restore(s, tag, ijk, t);
+    }
 };
-
-// StepSchedule::step, sampling.hpp:36-38
-template <int Sched>
-__device__ __forceinline__ double sched_step(const SamplerDev& s, double t) {
-    if constexpr (Sched == SOGK_CONSTANT_SCHED)
-        return s.dt0;
-    else
-        return std_max(s.dt0, s.growth * t);
-}
 
 __device__ __forceinline__ uint32_t pack_cell(const int ijk[3]) {
     return (uint32_t)(ijk[0] & 1023) | ((uint32_t)(ijk[1] & 1023) << 10) |
            ((uint32_t)(ijk[2] & 1023) << 20);
 }
 
-// sample_branch / sample_skip, sampling.hpp:87-122.  Sink::emit(t, t_next, ev)
-// returns false to stop early (the write pass stops once the ray's count is
-// written).  kernel_lookups counts probe calls like the reference probes.
-template <bool Branch, int Sched, class An, class Sink>
-__device__ __forceinline__ void run_kernel(An& an, const SamplerDev& s, Sink& sink,
-                                           int& kernel_lookups) {
-    if (!an.valid()) return;
-    const double t_end = an.t_exit();
-    double t_last = an.t_enter();
-    Event ev;
-    while (t_last <= t_end) {
-        if (!an.next(s, ev)) break;
-        if (!Branch && !ev.occ) continue;
-        while (t_last <= ev.t0) t_last += sched_step<Sched>(s, t_last);
-        while (t_last <= ev.t1) {
-            const double nx = t_last + sched_step<Sched>(s, t_last);
-            bool emit = true;
-            if (Branch) {
-                ++kernel_lookups;
-                emit = an.probe(s, ev);
-            }
-            if (emit && !sink.emit(t_last, nx, ev)) return;
-            t_last = nx;
-        }
+// A run: the ladder points one event contributes, S[first .. first + n).
+struct Run {
+    double first;  // first ladder point > ev.t0
+    int n;         // ladder points in (ev.t0, ev.t1]
+    uint32_t cell;
+    uint8_t level; // Level | grid_level << 2
+    // resume point of the event (written by pass 1 for the ray's first run)
+    int ijk[3];
+    int tag;
+    double t0, t_last0;
+};
+
+// Per-ray resume state of pass 2: restarting the analyzer at the event that
+// produced the ray's first run, with the ladder where it stood before it.
+struct Resume {
+    int ijk[3];
+    int tag;    // cascade segment
+    double t_cur;
+    double t_last;
+};
+
+// sample_branch / sample_skip (sampling.hpp:87-122) as a generator of runs.
+// Identical control flow to the reference kernels -- the outer loop pulls an
+// event while t_last <= t_exit, the skip kernel ignores unoccupied events, the
+// branch kernel walks all of them -- but the ladder is advanced per event in
+// closed form (sogk_ladder.cuh) instead of point by point.  The branch
+// kernel's per-point probe returns the same answer for every point of an
+// event (same ijk), so it is evaluated once per event and counted n times
+// (kernel_lookups), exactly as many probes as the reference makes.
+template <bool Branch, int Sched, class An>
+struct RunGen {
+    An an;
+    double t_last, t_end;
+    int kernel_lookups;
+    bool alive;
+    bool stalled;
+
+    __device__ __forceinline__ void init(const Ray& r, const SamplerDev& s) {
+        an.init(r, s);
+        kernel_lookups = 0;
+        stalled = false;
+        alive = an.valid();
+        t_last = an.t_enter();
+        t_end = an.t_exit();
     }
-}
+
+    // One analyzer call (one event):
+    // 0 = ray finished, 1 = event without samples, 2 = `run` holds the event's samples.
+    __device__ __forceinline__ int step(const SamplerDev& s, Run& run) {
+        if (!(alive && t_last <= t_end)) {
+            alive = false;
+            return 0;
+        }
+        Event ev;
+        const int got = an.next(s, ev);
+        if (got == 0) {
+            alive = false;
+            return 0;
+        }
+        if (got < 0) return 1; // analyzer-internal iteration, no event yet
+        if (!Branch && !ev.occ) return 1;
+        const double t_last0 = t_last;
+        ladder_seek<Sched>(t_last, ev.t0, s.dt0, s.inv_dt0, s.growth, s.t_switch, stalled);
+        const double first = t_last;
+        const int n = (int)ladder_seek<Sched>(t_last, ev.t1, s.dt0, s.inv_dt0, s.growth, s.t_switch, stalled);
+        if (stalled) {
+            alive = false;
+            return 0;
+        }
+        bool occ = ev.occ;
+        if (Branch) {
+            kernel_lookups += n;
+            if (n > 0) occ = an.probe(s, ev);
+        }
+        if (n > 0 && occ) {
+            run.first = first;
+            run.n = n;
+            run.cell = pack_cell(ev.ijk);
+            run.level = (uint8_t)(ev.level | (ev.grid_level << 2));
+            run.ijk[0] = ev.ijk[0];
+            run.ijk[1] = ev.ijk[1];
+            run.ijk[2] = ev.ijk[2];
+            run.tag = an.resume_tag();
+            run.t0 = ev.t0;
+            run.t_last0 = t_last0;
+            return 2;
+        }
+        return 1;
+    }
+
+    // next run with n >= 1 samples; false at the end of the ray
+    __device__ __forceinline__ bool next(const SamplerDev& s, Run& run) {
+        int st;
+        while ((st = step(s, run)) == 1) {
+        }
+        return st == 2;
+    }
+
+    __device__ __forceinline__ void resume(const SamplerDev& s, const Resume& r) {
+        if (!alive) return;
+        an.restore(s, r.tag, r.ijk, r.t_cur);
+        t_last = r.t_last;
+    }
+
+    __device__ __forceinline__ bool undefined() const { return an.undefined() || stalled; }
+};
 
 } // namespace sogk

@@ -17,12 +17,16 @@ struct Variant {
 
 cudaError_t launch_count(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, int64_t* packed,
-                         int64_t* stats, uint8_t* status, int32_t* counters, uint64_t* tiles,
-                         unsigned int* ctr, cudaStream_t st);
+                         int64_t* stats, uint8_t* status, int32_t* counters, void* resume,
+                         unsigned long long* ray_ctr, cudaStream_t st); // ray_ctr != NULL: persistent
+cudaError_t launch_scan(int64_t n, int64_t* packed, int64_t* stats, uint64_t* tiles,
+                        unsigned int* ctr, cudaStream_t st);
+int64_t scan_tiles(int64_t n);
+size_t resume_bytes(int64_t n);
 cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, const int64_t* packed,
-                         int64_t base, double* ts, double* te, int32_t* ri, uint32_t* ce,
-                         uint8_t* lv, cudaStream_t st);
+                         const void* resume, int64_t base, double* ts, double* te, int32_t* ri,
+                         uint32_t* ce, uint8_t* lv, unsigned long long* ray_ctr, cudaStream_t st);
 cudaError_t launch_raygen(const CameraDev& cam, int64_t first, int64_t n, double* rays,
                           cudaStream_t st);
 

@@ -30,6 +30,8 @@ struct GridDev {
     int res[3];
     double wmin[3];
     double voxel;
+    double inv_voxel;      // 1/voxel
+    int voxel_pow2;        // voxel is a power of two: x / voxel == x * inv_voxel exactly
     double clo[3], chi[3]; // voxel-centre bounds (center_bounds, sampling.hpp:248-251)
     const uint8_t* bits;   // dense payload
     int R[3];              // regions per axis
@@ -45,6 +47,9 @@ struct SamplerDev {
     int n_levels;
     int spin_cap;
     double dt0, growth;
+    double inv_dt0;  // 1/dt0, jump-length estimates only
+    int refill_min;  // persistent kernels: refill when at least this many lanes are idle
+    double t_switch; // linear schedule: largest t with fl(growth * t) <= dt0 (DBL_MAX if growth == 0)
 };
 
 struct CameraDev {
