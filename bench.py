@@ -32,6 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(1, os.path.join(ROOT, "tests"))  # oracle_bindings: CPU-baseline leg only
 
+from paper_2404_10272_b200.shard import broadcast_payload, view_of  # noqa: E402
+
 CAM_POS = (1.9, 1.4, 2.3)
 N_VIEWS = 200
 
@@ -165,9 +167,9 @@ class Workload:
             h = P.make_probe_rays(t, self.n_probe, seed=1000 + step_index * world + rank)
             out.copy_(torch.from_numpy(h))
             return
-        view = (step_index * world + rank) + obj * (N_VIEWS // max(1, len(self.objects)))
-        if self.name in ("cfg1", "cfg3") and step_index * world + rank == 0:
-            view = 0
+        view = view_of(step_index, rank, world, N_VIEWS, obj * (N_VIEWS // max(1, len(self.objects))))
+        if self.name in ("cfg1", "cfg3"):
+            view = 0  # the bench camera pose of the config
         cam = orbit_camera(P, view, self.width, self.height)
         cam.rays_device(0, self.width * self.height, out=out)
 
@@ -176,9 +178,9 @@ class Workload:
         if self.name == "cfg4":
             t = self.objects[0]["levels"][0][0]
             return P.make_probe_rays(t, self.n_probe, seed=1000 + step_index * world + rank)
-        view = (step_index * world + rank) + obj * (N_VIEWS // max(1, len(self.objects)))
-        if self.name in ("cfg1", "cfg3") and step_index * world + rank == 0:
-            view = 0
+        view = view_of(step_index, rank, world, N_VIEWS, obj * (N_VIEWS // max(1, len(self.objects))))
+        if self.name in ("cfg1", "cfg3"):
+            view = 0  # the bench camera pose of the config
         return orbit_camera(P, view, self.width, self.height).rays()
 
 
@@ -214,8 +216,7 @@ def run_gpu(args):
         dense_lv, vdb_lv = [], []
         for t, bits in o["levels"]:
             d_bits = torch.from_numpy(bits).to(dev)
-            if world > 1:
-                dist.broadcast(d_bits, src=0)
+            broadcast_payload(d_bits)  # once, NCCL over NVLink; rank 0's payload wins
             dg = P.DenseGrid(t, d_bits)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -582,7 +583,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])

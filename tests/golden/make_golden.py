@@ -27,8 +27,8 @@ def grid_arrays(prefix, g, out):
 def main():
     out = {}
     # 1) scenes (generate_scene) at 32^3/64^3 and their SOG1 bytes (build_sparse + serialize_sparse)
-    scenes = [("blobs", 32, 1, 0.05, 12), ("shell", 64, 1, 0.05, 12), ("sponge", 32, 2, 0.05, 12),
-              ("random", 32, 3, 0.1, 12), ("blobs", 64, 4, 0.05, 48)]
+    scenes = [("blobs", 32, 1, 0.05, 12), ("shell", 48, 1, 0.05, 12), ("sponge", 32, 2, 0.05, 12),
+              ("random", 32, 3, 0.1, 12), ("blobs", 40, 4, 0.05, 48)]
     for i, (kind, res, seed, frac, count) in enumerate(scenes):
         g = R.scene(kind, res, seed=seed, fraction=frac, count=count)
         grid_arrays(f"scene{i}", g, out)
@@ -36,19 +36,19 @@ def main():
         out[f"scene{i}_frac"] = np.float64(frac)
         out[f"scene{i}_sog1"] = np.frombuffer(R.sog1(g), np.uint8)
     # odd resolution + multi-region grids (padding, root entries)
-    for i, (res, seed, bf, nf) in enumerate([((11, 5, 9), 9, 0.4, 0.05), ((144, 8, 136), 77, 0.05, 0.001)]):
+    for i, (res, seed, bf, nf) in enumerate([((11, 5, 9), 9, 0.4, 0.05), ((136, 8, 130), 77, 0.05, 0.001)]):
         g = R.random_blocky_grid(res, (-1.0, -1.0, -1.0), 2.0 / res[0], seed, bf, nf)
         grid_arrays(f"blocky{i}", g, out)
         out[f"blocky{i}_args"] = np.array([seed, bf, nf], np.float64)
         out[f"blocky{i}_sog1"] = np.frombuffer(R.sog1(g), np.uint8)
     # 2) rays: random_ray, make_probe_rays, camera
     g0 = R.scene("blobs", 32, seed=1)
-    out["rays_random"] = R.random_rays(g0, 400, 7)
-    out["rays_probe"] = R.probe_rays(g0, 400, 11)
-    out["rays_camera"] = R.camera_rays(width=33, height=21)
+    out["rays_random"] = R.random_rays(g0, 200, 7)
+    out["rays_probe"] = R.probe_rays(g0, 200, 11)
+    out["rays_camera"] = R.camera_rays(width=21, height=15)
     # 3) sampler outputs through sog::run_sampler / run_cascade_sampler (+ recorded cells)
     cases = []
-    for si in (0, 1, 3):
+    for si in (0, 2, 3):
         for rays_name in ("rays_random", "rays_camera"):
             for an, k in ((DDA, BRANCH), (DDA, SKIP), (HDDA, BRANCH), (HDDA, SKIP)):
                 for sk, dt, gr in ((CONSTANT, 0.5 * 2.0 / out[f"scene{si}_res"][0], 0.0), (LINEAR, 0.011, 1.0 / 128)):
@@ -67,7 +67,7 @@ def main():
     lv = R.cascade("blobs", 4, 32, seed=1)
     for b, g in enumerate(lv):
         grid_arrays(f"casc{b}", g, out)
-    rays = R.random_rays(lv[-1], 300, 5)
+    rays = R.random_rays(lv[-1], 200, 5)
     out["casc_rays"] = rays
     for an, k in ((DDA, BRANCH), (HDDA, SKIP)):
         p = R.sampler(lv, an, k, LINEAR, 0.013, 1.0 / 256).sample(rays)
@@ -78,7 +78,7 @@ def main():
     for an in (DDA, HDDA):
         s = R.sampler([g], an, SKIP, CONSTANT, 0.03)
         evs, ts, ns = [], [], []
-        for r in out["rays_random"][:40]:
+        for r in out["rays_random"][:20]:
             n, ev, ctr = s.events(r)
             ns.append((n, ctr[0], ctr[1]))
             for e in ev:
