@@ -1,0 +1,258 @@
+// sogk_sog.hpp — C++ drop-in shim: the reference's own types and entry points
+// (namespace sog, /root/reference/proj/include/sog/) on top of the sm_100a
+// C-ABI (sogk.h).  Header-only; include it in code that already includes the
+// reference library and link libsogk.so:
+//
+//     #include <sog/sog.hpp>
+//     #include "sogk_sog.hpp"
+//     sog::gpu::DeviceSparseGrid vdb = sog::gpu::build_sparse(dense);        // sparse.hpp:333
+//     sog::gpu::Sampler hdda(vdb, sog::KernelKind::skip, sched);             // make_sampler, bench.hpp:382
+//     sog::gpu::PackedSamples out = hdda.sample_rays(rays);                  // batched run_sampler
+//     sog::SampleRun one = hdda(ray);                                        // run_sampler, sampling.hpp:182
+//
+// Errors follow the reference: std::invalid_argument for bad arguments,
+// sog::io_error for SOG0/SOG1 problems, std::runtime_error for device failures.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sog/io.hpp"
+#include "sog/sampling.hpp"
+#include "sogk.h"
+
+namespace sog::gpu {
+
+static_assert(sizeof(Ray) == 8 * sizeof(double), "sog::Ray must be 8 packed doubles");
+
+inline void check(int status) {
+    if (status == SOGK_OK) return;
+    char buf[512];
+    sogk_last_error(buf, sizeof buf);
+    const std::string msg(buf);
+    switch (status) {
+        case SOGK_INVALID_ARG: throw std::invalid_argument(msg);
+        case SOGK_IO_ERROR: {
+            io_errc c = io_errc::corrupt;
+            if (msg.find("bad magic") != std::string::npos) c = io_errc::bad_magic;
+            else if (msg.find("bad version") != std::string::npos) c = io_errc::bad_version;
+            else if (msg.find("truncated") != std::string::npos) c = io_errc::truncated;
+            throw io_error(c, msg);
+        }
+        default: throw std::runtime_error(std::string(sogk_status_string(status)) + ": " + msg);
+    }
+}
+
+inline sogk_transform to_c(const GridTransform& t) {
+    sogk_transform c{};
+    for (int a = 0; a < 3; ++a) {
+        c.res[a] = t.resolution[a];
+        c.world_min[a] = t.world_min[a];
+    }
+    c.voxel_size = t.voxel_size;
+    return c;
+}
+
+struct GridDeleter {
+    void operator()(sogk_grid* g) const { sogk_grid_destroy(g); }
+};
+using GridHandle = std::shared_ptr<sogk_grid>;
+
+/// DenseGrid (grid.hpp:120-165) resident in HBM.
+class DeviceDenseGrid {
+public:
+    explicit DeviceDenseGrid(const DenseGrid& d, void* stream = nullptr) : t_(d.transform()) {
+        const sogk_transform c = to_c(t_);
+        sogk_grid* g = nullptr;
+        check(sogk_grid_create_dense(&c, d.payload().data(), d.payload().size(), stream, &g));
+        h_.reset(g, GridDeleter{});
+    }
+    const GridTransform& transform() const { return t_; }
+    sogk_grid* handle() const { return h_.get(); }
+    DenseGrid to_host() const {
+        DenseGrid d(t_);
+        check(sogk_grid_download_dense(h_.get(), d.payload().data(), d.payload().size()));
+        return d;
+    }
+
+private:
+    GridTransform t_;
+    GridHandle h_;
+};
+
+/// SparseGrid (sparse.hpp:141-218) as the GPU VDB layout.
+class DeviceSparseGrid {
+public:
+    DeviceSparseGrid(sogk_grid* g, const GridTransform& t) : t_(t), h_(g, GridDeleter{}) {}
+    const GridTransform& transform() const { return t_; }
+    sogk_grid* handle() const { return h_.get(); }
+    sogk_grid_info info() const {
+        sogk_grid_info i{};
+        check(sogk_grid_get_info(h_.get(), &i));
+        return i;
+    }
+    std::size_t leaf_count() const { return std::size_t(info().leaf_count); }
+    std::size_t memory_bytes() const { return std::size_t(info().memory_bytes); } // io.hpp:227
+    /// serialize_sparse (io.hpp:161-181): byte-identical to the reference tree's SOG1
+    std::vector<std::uint8_t> serialize() const {
+        std::size_t n = 0;
+        check(sogk_grid_export_sog1(h_.get(), nullptr, &n));
+        std::vector<std::uint8_t> out(n);
+        check(sogk_grid_export_sog1(h_.get(), out.data(), &n));
+        return out;
+    }
+    /// the reference tree itself (deserialize_sparse of the exported bytes)
+    SparseGrid to_host() const { return deserialize_sparse(serialize()); }
+
+private:
+    GridTransform t_;
+    GridHandle h_;
+};
+
+/// build_sparse (sparse.hpp:333-371) on the GPU.
+inline DeviceSparseGrid build_sparse(const DeviceDenseGrid& d, void* stream = nullptr) {
+    sogk_grid* g = nullptr;
+    check(sogk_grid_build_vdb(d.handle(), stream, &g));
+    return DeviceSparseGrid(g, d.transform());
+}
+inline DeviceSparseGrid build_sparse(const DenseGrid& d, void* stream = nullptr) {
+    return build_sparse(DeviceDenseGrid(d, stream), stream);
+}
+
+/// Packed sample intervals of a ray batch (sogk.h output contract).
+struct PackedSamples {
+    std::vector<std::int64_t> packed_info; // [n][2] offset, count
+    std::vector<double> t_starts, t_ends;
+    std::vector<std::int32_t> ray_indices;
+    std::vector<std::uint32_t> cells;
+    std::vector<std::uint8_t> levels;
+    std::vector<std::uint8_t> status;
+    std::vector<std::int32_t> counters; // [n][3]
+    std::int64_t stats[SOGK_STATS_LEN] = {};
+
+    std::size_t size() const { return packed_info.size() / 2; }
+    /// the reference SampleBuffer of ray r (sampling.hpp:42)
+    SampleBuffer samples(std::size_t r) const {
+        const auto off = packed_info[2 * r], cnt = packed_info[2 * r + 1];
+        return SampleBuffer(t_starts.begin() + off, t_starts.begin() + off + cnt);
+    }
+    /// the reference SampleRun of ray r (sampling.hpp:157-164)
+    SampleRun run(std::size_t r) const {
+        SampleRun out;
+        out.samples = samples(r);
+        out.analyzer_lookups = counters[3 * r];
+        out.analyzer_steps = counters[3 * r + 1];
+        out.kernel_lookups = counters[3 * r + 2];
+        return out;
+    }
+};
+
+struct SamplerDeleter {
+    void operator()(sogk_sampler* s) const { sogk_sampler_destroy(s); }
+};
+
+/// One variant of the reference's variant matrix (bench.hpp:30-64): dense+dda+{branch,skip}
+/// or sparse+hdda+{branch,skip}, over one grid or a cascade (sampling.hpp:222-462).
+class Sampler {
+public:
+    Sampler(const DeviceDenseGrid& g, KernelKind k, const StepSchedule& s)
+        : Sampler({g.handle()}, SOGK_DDA, k, s, false) {}
+    Sampler(const DeviceSparseGrid& g, KernelKind k, const StepSchedule& s)
+        : Sampler({g.handle()}, SOGK_HDDA, k, s, false) {}
+    Sampler(const std::vector<DeviceDenseGrid>& cascade, KernelKind k, const StepSchedule& s)
+        : Sampler(handles(cascade), SOGK_DDA, k, s, true) {}
+    Sampler(const std::vector<DeviceSparseGrid>& cascade, KernelKind k, const StepSchedule& s)
+        : Sampler(handles(cascade), SOGK_HDDA, k, s, true) {}
+
+    /// Batched run_sampler / run_cascade_sampler: host rays in, host packed samples out.
+    PackedSamples sample_rays(std::span<const Ray> rays, std::int64_t ray_index_base = 0,
+                              void* stream = nullptr) const {
+        const std::int64_t n = std::int64_t(rays.size());
+        PackedSamples out;
+        out.packed_info.resize(2 * n);
+        out.status.resize(n);
+        out.counters.resize(3 * n);
+        std::int64_t cap = std::max<std::int64_t>(1024, 64 * n);
+        for (;;) {
+            out.t_starts.resize(cap);
+            out.t_ends.resize(cap);
+            out.ray_indices.resize(cap);
+            out.cells.resize(cap);
+            out.levels.resize(cap);
+            const int st = sogk_sample_host(
+                s_.get(), reinterpret_cast<const double*>(rays.data()), n, ray_index_base, cap,
+                out.packed_info.data(), out.t_starts.data(), out.t_ends.data(), out.ray_indices.data(),
+                out.cells.data(), out.levels.data(), out.status.data(), out.counters.data(), out.stats,
+                stream);
+            if (st == SOGK_INSUFFICIENT_CAPACITY) {
+                cap = out.stats[SOGK_STAT_TOTAL_SAMPLES];
+                continue;
+            }
+            check(st);
+            break;
+        }
+        const std::size_t total = std::size_t(out.stats[SOGK_STAT_TOTAL_SAMPLES]);
+        out.t_starts.resize(total);
+        out.t_ends.resize(total);
+        out.ray_indices.resize(total);
+        out.cells.resize(total);
+        out.levels.resize(total);
+        if (out.stats[SOGK_STAT_INVALID_RAYS])
+            throw std::invalid_argument("ray direction must be unit length and 0 <= t_min < t_max");
+        if (out.stats[SOGK_STAT_UNDEFINED_RAYS])
+            throw std::runtime_error("reference HDDA does not terminate on some rays (edge-crossing spin)");
+        return out;
+    }
+
+    /// run_sampler for one ray (drop-in; prefer sample_rays for throughput)
+    SampleRun operator()(const Ray& ray) const { return sample_rays({&ray, 1}).run(0); }
+
+    sogk_sampler* handle() const { return s_.get(); }
+
+private:
+    template <class G>
+    static std::vector<sogk_grid*> handles(const std::vector<G>& gs) {
+        std::vector<sogk_grid*> h;
+        for (const auto& g : gs) h.push_back(g.handle());
+        return h;
+    }
+    Sampler(std::vector<sogk_grid*> levels, int analyzer, KernelKind k, const StepSchedule& s,
+            bool cascade) {
+        sogk_sampler_desc d{};
+        d.analyzer = analyzer;
+        d.kernel = k == KernelKind::branch ? SOGK_BRANCH : SOGK_SKIP;
+        d.schedule = s.kind == StepSchedule::Kind::constant ? SOGK_CONSTANT : SOGK_LINEAR;
+        d.dt0 = s.dt0;
+        d.growth = s.growth;
+        d.cascade = cascade ? 1 : 0;
+        sogk_sampler* h = nullptr;
+        check(sogk_sampler_create(const_cast<const sogk_grid* const*>(levels.data()),
+                                  int(levels.size()), &d, &h));
+        s_.reset(h, SamplerDeleter{});
+    }
+    std::shared_ptr<sogk_sampler> s_;
+};
+
+/// run_sampler overloads (sampling.hpp:166-196) over device grids
+inline SampleRun run_sampler(const Ray& ray, const DeviceDenseGrid& g, KernelKind k,
+                             const StepSchedule& s) {
+    return Sampler(g, k, s)(ray);
+}
+inline SampleRun run_sampler(const Ray& ray, const DeviceSparseGrid& g, KernelKind k,
+                             const StepSchedule& s) {
+    return Sampler(g, k, s)(ray);
+}
+
+/// make_sampler (bench.hpp:382-413) for the GPU variants: the std::function the
+/// reference's render_frame / run_matrix consume.
+inline std::function<SampleRun(const Ray&)> make_sampler(const Sampler& s) {
+    return [s](const Ray& r) { return s(r); };
+}
+
+} // namespace sog::gpu

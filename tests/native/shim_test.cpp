@@ -1,0 +1,93 @@
+// Drop-in check of include/sogk_sog.hpp: the unmodified reference library
+// (sog::run_sampler, sog::build_sparse + serialize_sparse) against sog::gpu on
+// the same inputs.  Built by oracle/Makefile into oracle/_ref/shim_test (it
+// compiles the reference headers, so it is test infrastructure); run by
+// tests/test_gpu_shim.py on the GPU box.  Exit 0 = bit-exact everywhere.
+#include <cstdio>
+#include <vector>
+
+#include "sog/sog.hpp"
+#include "sogk_sog.hpp"
+
+using namespace sog;
+
+static int failures = 0;
+#define EXPECT(c, ...)                           \
+    do {                                         \
+        if (!(c)) {                              \
+            ++failures;                          \
+            std::printf("FAIL: " __VA_ARGS__);   \
+            std::printf("\n");                   \
+        }                                        \
+    } while (0)
+
+int main() {
+    const GridTransform t = GridTransform::cube(64, {-1, -1, -1}, 2.0);
+    SceneParams p;
+    p.seed = 1;
+    const GeneratedScene gen = generate_scene(SceneKind::shell, t, p);
+    const DenseGrid& dense = gen.grid;
+    const SparseGrid sparse = build_sparse(dense);
+
+    // GPU build == reference build, byte for byte (io.hpp:161-181)
+    gpu::DeviceDenseGrid ddense(dense);
+    gpu::DeviceSparseGrid dvdb = gpu::build_sparse(ddense);
+    EXPECT(dvdb.serialize() == serialize_sparse(sparse), "SOG1 bytes differ");
+    EXPECT(dvdb.memory_bytes() == memory_bytes(sparse), "memory_bytes differ");
+    EXPECT(dvdb.leaf_count() == sparse.leaf_count(), "leaf_count differs");
+    EXPECT(dvdb.to_host().structurally_equal(sparse), "round trip differs");
+
+    Camera cam;
+    cam.position = {1.9, 1.4, 2.3};
+    cam.vfov_deg = 42.0;
+    cam.width = 80;
+    cam.height = 60;
+    std::vector<Ray> rays;
+    for (int y = 0; y < cam.height; ++y)
+        for (int x = 0; x < cam.width; ++x) rays.push_back(cam.pixel_ray(x, y));
+
+    const StepSchedule scheds[] = {StepSchedule::constant(0.5 * t.voxel_size),
+                                   StepSchedule::linear(0.011, 1.0 / 128.0)};
+    for (const auto& sched : scheds)
+        for (KernelKind k : {KernelKind::branch, KernelKind::skip}) {
+            const gpu::Sampler sd(ddense, k, sched), sh(dvdb, k, sched);
+            const gpu::PackedSamples od = sd.sample_rays(rays), oh = sh.sample_rays(rays);
+            long mism = 0;
+            for (std::size_t r = 0; r < rays.size(); ++r) {
+                const SampleRun rd = run_sampler(rays[r], dense, k, sched);
+                const SampleRun rh = run_sampler(rays[r], sparse, k, sched);
+                const SampleRun gd = od.run(r), gh = oh.run(r);
+                mism += gd.samples != rd.samples || gd.analyzer_lookups != rd.analyzer_lookups ||
+                        gd.analyzer_steps != rd.analyzer_steps || gd.kernel_lookups != rd.kernel_lookups;
+                mism += gh.samples != rh.samples || gh.analyzer_lookups != rh.analyzer_lookups ||
+                        gh.analyzer_steps != rh.analyzer_steps || gh.kernel_lookups != rh.kernel_lookups;
+            }
+            EXPECT(mism == 0, "%ld ray mismatches (kernel %d)", mism, int(k));
+        }
+    // single-ray drop-in
+    const gpu::Sampler one(dvdb, KernelKind::skip, scheds[0]);
+    EXPECT(one(rays[1234]).samples == run_sampler(rays[1234], sparse, KernelKind::skip, scheds[0]).samples,
+           "single-ray run_sampler differs");
+    // cascade (run_cascade_sampler, sampling.hpp:440-455)
+    const DenseCascade dc = build_dense_cascade(gen.scene, t, 3, p.threshold);
+    const SparseCascade sc = build_sparse_cascade(dc);
+    std::vector<gpu::DeviceSparseGrid> gl;
+    for (const auto& l : dc.levels) gl.push_back(gpu::build_sparse(l));
+    const StepSchedule lin = StepSchedule::linear(0.5 * t.voxel_size, 1.0 / 256.0);
+    const gpu::PackedSamples oc = gpu::Sampler(gl, KernelKind::skip, lin).sample_rays(rays);
+    long cm = 0;
+    for (std::size_t r = 0; r < rays.size(); ++r)
+        cm += oc.samples(r) != run_cascade_sampler(rays[r], sc, KernelKind::skip, lin).samples;
+    EXPECT(cm == 0, "%ld cascade ray mismatches", cm);
+    // errors like the reference
+    bool threw = false;
+    try {
+        gpu::Sampler bad(dvdb, KernelKind::skip, StepSchedule{StepSchedule::Kind::constant, -1.0, 0.0});
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    EXPECT(threw, "negative step did not throw std::invalid_argument");
+    std::printf("%s: %zu rays x 4 variants x 2 schedules + cascade, %d failures\n",
+                failures ? "FAILED" : "OK", rays.size(), failures);
+    return failures ? 1 : 0;
+}
