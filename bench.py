@@ -69,48 +69,52 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + throttle reasons sampled through NVML every 5 ms while the timed region runs
+    (nvidia-smi's own polling starts too slowly for a sub-second region); falls back to
+    `nvidia-smi -lms` when NVML is unavailable."""
+
+    # nvmlClocksEventReasons bits (nvml.h)
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.max_mhz = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.rows.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), int(get_r(h))))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([s.strip() for s in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t is not None:
+            self.t.join(timeout=1)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, m in self.rows for b, name in self.BITS.items() if m & b})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------
@@ -404,10 +408,10 @@ def run_gpu(args):
     # roofline: dominant kernel (larger share of the step) with its algorithmic bytes
     launches = args.steps * n_obj
     nr_loc = nr * n_obj * args.steps
-    write_bytes = nr_loc * 16 + h["hit_rays"] * 64 + h["local_samples"] * 24
+    write_bytes = nr_loc * 16 + h["local_samples"] * 24  # packed_info read + samples written
     count_bytes = nr_loc * (64 + 16)
     if h["write_ms"] >= h["count_ms"]:
-        dom, dom_ms, dom_bytes = "write_kernel (pass 2)", h["write_ms"], write_bytes
+        dom, dom_ms, dom_bytes = "expand_kernel + tail_kernel (pass 2)", h["write_ms"], write_bytes
     else:
         dom, dom_ms, dom_bytes = "count_kernel (pass 1 + fused scan)", h["count_ms"], count_bytes
     achieved = dom_bytes / launches / (dom_ms / launches / 1e3) / 1e9
@@ -454,7 +458,7 @@ def run_gpu(args):
                           "basis": "N_rays*(64+16) + N_samples*24 + VDB bytes (SURVEY §8d)"},
         "vdb_build_ms": build_ms,
         "grid_bytes": {"dense": dense_bytes, "vdb_sog1": vdb_bytes},
-        "gpu_launches": 2 * launches,
+        "gpu_launches": 4 * launches,  # count, scan, expand, tail per object
         "clocks": h["clocks"],
     }
     if e2e:

@@ -78,6 +78,7 @@ enum {
     SOGK_STAT_ANALYZER_LOOKUPS = 3, /* sum of SampleRun::analyzer_lookups */
     SOGK_STAT_ANALYZER_STEPS = 4,   /* sum of SampleRun::analyzer_steps */
     SOGK_STAT_KERNEL_LOOKUPS = 5,   /* sum of SampleRun::kernel_lookups */
+    SOGK_STAT_SLAB_OVERFLOW_RAYS = 6, /* rays whose samples overflowed the pass-1 slab (diagnostic) */
     SOGK_STATS_LEN = 8
 };
 

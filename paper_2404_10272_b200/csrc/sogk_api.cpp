@@ -173,15 +173,26 @@ struct sogk_sampler {
         cudaFree(hb);
     }
 
-    // pass 1 -> pass 2 handshake: the resume states of the last count call
+    // pass 1 -> pass 2 handshake: the sample slabs of the last count call
     const void* last_rays = nullptr;
     int64_t last_first = -1, last_n = -1;
     bool last_cam = false;
-    bool persistent = false; // SOGK_PERSISTENT=1 selects the persistent-thread kernels (slower here)
+    int64_t slab_cap = 256; // C: slab entries per ray (SOGK_SLAB; 0 = resume-only)
 
-    // workspace = [scan tile states | tile counter | resume states]
+    // workspace = [scan tile states | counters (64 B) | resume states | overflow list | slabs]
+    int64_t cap_for(int64_t n) const {
+        // keep the slabs below ~24 GiB of HBM; a smaller slab only sends more rays to tail_kernel
+        int64_t c = slab_cap;
+        while (c > 0 && double(n) * double(c) * 13.0 > 24.0 * (1ull << 30)) c -= 8;
+        return c < 0 ? 0 : c;
+    }
+    static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+    size_t need_bytes(int64_t n) const {
+        const size_t e = size_t(n) * size_t(cap_for(n));
+        return scan_off(n) + al(resume_bytes(n)) + al(size_t(n) * 4) + al(e * 8) + al(e * 4) + al(e);
+    }
     int ensure_ws(int64_t n) {
-        const size_t need = scan_off(n) + resume_bytes(n);
+        const size_t need = need_bytes(n);
         if (need <= ws_bytes) return SOGK_OK;
         cudaFree(ws);
         ws = nullptr;
@@ -192,12 +203,26 @@ struct sogk_sampler {
         return SOGK_OK;
     }
     static size_t scan_off(int64_t n) { return ((size_t(scan_tiles(n)) * 8 + 64 + 255) / 256) * 256; }
-    // [tiles | scan ctr (8B) | count ray ctr (8B) | write ray ctr (8B)]
-    unsigned long long* ray_ctr(int64_t n, int which) const {
-        return reinterpret_cast<unsigned long long*>(tiles() + scan_tiles(n) + 1 + which);
-    }
     uint64_t* tiles() const { return static_cast<uint64_t*>(ws); }
-    void* resume(int64_t n) const { return static_cast<char*>(ws) + scan_off(n); }
+    // counters: [scan tile counter (u32 in a u64 slot) | overflow counter]
+    unsigned* ovf_ctr(int64_t n) const { return reinterpret_cast<unsigned*>(tiles() + scan_tiles(n) + 1); }
+    SlabDev slab(int64_t n) const {
+        char* p = static_cast<char*>(ws) + scan_off(n);
+        SlabDev S{};
+        S.C = cap_for(n);
+        const size_t e = size_t(n) * size_t(S.C);
+        S.resume = reinterpret_cast<Resume*>(p);
+        p += al(resume_bytes(n));
+        S.ovf_list = reinterpret_cast<uint32_t*>(p);
+        p += al(size_t(n) * 4);
+        S.t = reinterpret_cast<double*>(p);
+        p += al(e * 8);
+        S.cell = reinterpret_cast<uint32_t*>(p);
+        p += al(e * 4);
+        S.lvl = reinterpret_cast<uint8_t*>(p);
+        S.ovf_ctr = ovf_ctr(n);
+        return S;
+    }
 };
 
 // ---------------------------------------------------------------------------
@@ -768,9 +793,7 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     s->v.cascade = cascade ? 1 : 0;
     s->v.branch = desc->kernel == SOGK_BRANCH ? 1 : 0;
     s->v.linear = desc->schedule == SOGK_LINEAR ? 1 : 0;
-    if (const char* e = std::getenv("SOGK_PERSISTENT")) s->persistent = std::atoi(e) != 0;
-    s->dev.refill_min = 1;
-    if (const char* e = std::getenv("SOGK_REFILL")) s->dev.refill_min = std::max(1, std::min(32, std::atoi(e)));
+    if (const char* e = std::getenv("SOGK_SLAB")) s->slab_cap = std::max(0, std::atoi(e));
     for (int b = 0; b < n_levels; ++b) s->dev.lv[b] = levels[b]->dev();
     s->dev.n_levels = n_levels;
     s->dev.spin_cap = desc->spin_cap > 0 ? desc->spin_cap : SOGK_DEFAULT_SPIN_CAP;
@@ -827,9 +850,9 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     CK(cudaMemsetAsync(s->ws, 0, size_t(tiles) * 8 + 64, S(stream)), "workspace reset");
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
-    void* resume = s->resume(n);
+    const SlabDev slab = s->slab(n);
     CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
-                    d_status, d_counters, resume, s->persistent ? s->ray_ctr(n, 0) : nullptr, S(stream)),
+                    d_status, d_counters, slab, S(stream)),
        "count launch");
     CK(launch_scan(n, d_packed, d_stats, s->tiles(),
                    reinterpret_cast<unsigned int*>(s->tiles() + tiles), S(stream)),
@@ -869,19 +892,12 @@ static int write_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     if (!d_packed || !ts || (!cam && !d_rays)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
-    // resume states are valid when pass 1 ran on this sampler with the same rays
+    // the slabs are valid when pass 1 ran on this sampler with the same rays
     const bool same = s->last_n == n && s->last_cam == (cam != nullptr) &&
                       (cam ? s->last_first == first : s->last_rays == d_rays);
-    const void* resume = same ? s->resume(n) : nullptr;
-    unsigned long long* ctr = nullptr;
-    if (s->persistent) {
-        int st = s->ensure_ws(n);
-        if (st) return st;
-        ctr = s->ray_ctr(n, 1);
-        CK(cudaMemsetAsync(ctr, 0, 8, S(stream)), "write counter reset");
-    }
-    CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, resume, base,
-                    ts, te, ri, ce, lv, ctr, S(stream)),
+    const SlabDev slab = same ? s->slab(n) : SlabDev{};
+    CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed,
+                    same ? &slab : nullptr, base, ts, te, ri, ce, lv, S(stream)),
        "write launch");
     return SOGK_OK;
 }

@@ -688,14 +688,6 @@ struct Run {
     double t0, t_last0;
 };
 
-// Per-ray resume state of pass 2: restarting the analyzer at the event that
-// produced the ray's first run, with the ladder where it stood before it.
-struct Resume {
-    int ijk[3];
-    int tag;    // cascade segment
-    double t_cur;
-    double t_last;
-};
 
 // sample_branch / sample_skip (sampling.hpp:87-122) as a generator of runs.
 // Identical control flow to the reference kernels -- the outer loop pulls an

@@ -15,18 +15,32 @@ struct Variant {
     int linear;   // 1: linear schedule
 };
 
+// Pass 1 -> pass 2 state (sampler workspace): every ray's first samples in a fixed
+// per-ray slab of C entries (t, cell, level), the resume state of rays whose runs did not
+// all fit (Resume::tag bits 8.. = samples in the slab), and the list of those rays.
+struct SlabDev {
+    double* t;          // [n][C]
+    uint32_t* cell;     // [n][C]
+    uint8_t* lvl;       // [n][C]
+    int64_t C;          // slab entries per ray; 0 = no slab (every ray resumes in tail_kernel)
+    Resume* resume;     // [n]
+    uint32_t* ovf_list; // [n]
+    unsigned* ovf_ctr;  // [1], zeroed before pass 1
+};
+
 cudaError_t launch_count(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, int64_t* packed,
-                         int64_t* stats, uint8_t* status, int32_t* counters, void* resume,
-                         unsigned long long* ray_ctr, cudaStream_t st); // ray_ctr != NULL: persistent
+                         int64_t* stats, uint8_t* status, int32_t* counters, const SlabDev& slab,
+                         cudaStream_t st);
 cudaError_t launch_scan(int64_t n, int64_t* packed, int64_t* stats, uint64_t* tiles,
                         unsigned int* ctr, cudaStream_t st);
 int64_t scan_tiles(int64_t n);
 size_t resume_bytes(int64_t n);
+// slab == nullptr: cold path (no matching pass 1), traverse every ray from its start
 cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, const int64_t* packed,
-                         const void* resume, int64_t base, double* ts, double* te, int32_t* ri,
-                         uint32_t* ce, uint8_t* lv, unsigned long long* ray_ctr, cudaStream_t st);
+                         const SlabDev* slab, int64_t base, double* ts, double* te, int32_t* ri,
+                         uint32_t* ce, uint8_t* lv, cudaStream_t st);
 cudaError_t launch_raygen(const CameraDev& cam, int64_t first, int64_t n, double* rays,
                           cudaStream_t st);
 

@@ -52,6 +52,15 @@ struct SamplerDev {
     double t_switch; // linear schedule: largest t with fl(growth * t) <= dt0 (DBL_MAX if growth == 0)
 };
 
+// Per-ray resume state of pass 2: restarting the analyzer at the event that
+// produced a run, with the ladder where it stood before it.
+struct Resume {
+    int ijk[3];
+    int tag;    // cascade segment
+    double t_cur;
+    double t_last;
+};
+
 struct CameraDev {
     double position[3], forward[3], right[3], cam_up[3];
     double tan_half, aspect, t_far;

@@ -3,13 +3,18 @@
 // Pass 1 (count_kernel): one thread per ray runs the analyzer with the
 // reference kernel's control flow (sample_skip / sample_branch over
 // Dda/Hdda/CascadeTraversal, sampling.hpp:87-122, 166-196, 305-455), advancing
-// the ladder per event in closed form; it writes the per-ray count, status,
-// counters and the resume state at the ray's first sample run.
+// the ladder per event in closed form.  It writes the per-ray count, status and
+// counters, and the ray's first samples (t, cell, level) into the ray's fixed
+// slab; a ray whose runs do not all fit stores the resume state of the first
+// run that did not.
 // Scan (scan_kernel): packed_info offsets = exclusive scan of the counts.
-// Pass 2 (write_kernel): rays with samples restart from their resume state,
-// regenerate the runs and stage samples in shared memory; each warp flushes
-// its staged samples with consecutive threads on consecutive output indices.
+// Pass 2 (gather_kernel): moves the slabs into the packed arrays, one output
+// sample per thread, every store coalesced; tail_kernel resumes the traversal
+// only for the rays whose slab overflowed.  write_kernel is the cold path (a
+// write with no matching pass 1): it traverses from the ray's start.
 #include <cuda_runtime.h>
+
+#include <climits>
 
 #include "sogk_device.cuh"
 #include "sogk_internal.h"
@@ -18,6 +23,9 @@ namespace sogk {
 
 constexpr int kBlock = 128;
 constexpr int kWriteBlock = 128;
+#ifndef SOGK_COUNT_MINB
+#define SOGK_COUNT_MINB 1 // pass-1 min resident blocks per SM (register cap), A/B-tunable
+#endif
 
 // ---------------------------------------------------------------------------
 // ray sources
@@ -123,12 +131,13 @@ __device__ __forceinline__ long long block_sum(long long v) {
     return t;
 }
 
-__device__ __forceinline__ void store_resume(Resume* dst, const Run& run) {
+// resume state at `run`; tag bits 8.. carry the number of samples already in the slab
+__device__ __forceinline__ void store_resume(Resume* dst, const Run& run, int filled) {
     Resume r;
     r.ijk[0] = run.ijk[0];
     r.ijk[1] = run.ijk[1];
     r.ijk[2] = run.ijk[2];
-    r.tag = run.tag;
+    r.tag = run.tag | (filled << 8);
     r.t_cur = run.t0;
     r.t_last = run.t_last0;
     *dst = r;
@@ -138,7 +147,7 @@ __device__ __forceinline__ void store_resume(Resume* dst, const Run& run) {
 // pass 1: per-ray counts, status, counters, resume state
 // ---------------------------------------------------------------------------
 struct Stats5 {
-    long long inv = 0, und = 0, lk = 0, sp = 0, klk = 0;
+    long long inv = 0, und = 0, lk = 0, sp = 0, klk = 0, ovf = 0;
     __device__ __forceinline__ void flush(int64_t* stats) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -147,6 +156,7 @@ struct Stats5 {
             lk += __shfl_xor_sync(0xffffffffu, lk, o);
             sp += __shfl_xor_sync(0xffffffffu, sp, o);
             klk += __shfl_xor_sync(0xffffffffu, klk, o);
+            ovf += __shfl_xor_sync(0xffffffffu, ovf, o);
         }
         if ((threadIdx.x & 31) == 0) {
             unsigned long long* S = reinterpret_cast<unsigned long long*>(stats);
@@ -155,6 +165,7 @@ struct Stats5 {
             if (lk) atomicAdd(S + SOGK_STAT_ANALYZER_LOOKUPS, (unsigned long long)lk);
             if (sp) atomicAdd(S + SOGK_STAT_ANALYZER_STEPS, (unsigned long long)sp);
             if (klk) atomicAdd(S + SOGK_STAT_KERNEL_LOOKUPS, (unsigned long long)klk);
+            if (ovf) atomicAdd(S + SOGK_STAT_SLAB_OVERFLOW_RAYS, (unsigned long long)ovf);
         }
     }
 };
@@ -198,11 +209,15 @@ __device__ __forceinline__ void count_invalid(long long r, int64_t* packed, uint
     reinterpret_cast<longlong2*>(packed)[r] = make_longlong2(0, 0);
 }
 
+
+// ---------------------------------------------------------------------------
+// pass 1: per-ray counts, status, counters, slab samples, resume state
+// ---------------------------------------------------------------------------
 template <int AN, bool CASC, bool BR, int SCH, class Src>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, SOGK_COUNT_MINB)
     count_kernel(const SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
-                 int32_t* __restrict__ counters, Resume* __restrict__ resume) {
+                 int32_t* __restrict__ counters, const SlabDev S) {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     Stats5 acc;
     if (r < n) {
@@ -213,16 +228,41 @@ __global__ void __launch_bounds__(kBlock)
             RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
             gen.init(ray, s);
             long long c = 0;
+            int filled = 0;     // samples in the slab
+            bool ovf = S.C == 0; // slab closed: the rest comes from the resume state
+            bool stored = false;
             Run run;
             for (;;) { // one flat loop: one analyzer step per iteration
                 const int st = gen.step(s, run);
                 if (st == 0) break;
                 if (st == 2) {
-                    if (c == 0 && resume) store_resume(resume + r, run);
+                    if (!ovf) {
+                        if (filled + run.n <= S.C) {
+                            const int64_t base = r * S.C + filled;
+                            double t = run.first;
+                            for (int i = 0; i < run.n; ++i) {
+                                S.t[base + i] = t;
+                                S.cell[base + i] = run.cell;
+                                S.lvl[base + i] = run.level;
+                                t = t + ladder_step<SCH>(t, s.dt0, s.growth);
+                            }
+                            filled += run.n;
+                        } else {
+                            ovf = true;
+                        }
+                    }
+                    if (ovf && !stored) {
+                        store_resume(S.resume + r, run, filled);
+                        stored = true;
+                    }
                     c += run.n;
                 }
             }
             count_finish(gen, r, c, packed, status, counters, acc);
+            if (stored && c > 0 && !gen.undefined()) {
+                S.ovf_list[atomicAdd(S.ovf_ctr, 1u)] = (uint32_t)r;
+                ++acc.ovf;
+            }
         }
     }
     acc.flush(stats); // warp-level: no block barrier, finished warps leave at once
@@ -405,17 +445,18 @@ struct LaneWriter {
     }
 };
 
+
+// cold path: no pass-1 slabs for these rays, traverse from the start
 template <int AN, bool CASC, bool BR, int SCH, bool VEC, class Src>
 __global__ void __launch_bounds__(kWriteBlock)
     write_kernel(const SamplerDev s, const Src src, int64_t n, const int64_t* __restrict__ packed,
-                 const Resume* __restrict__ resume, int64_t ray_index_base, const Out o) {
+                 int64_t ray_index_base, const Out o) {
     const int64_t r = (int64_t)blockIdx.x * kWriteBlock + threadIdx.x;
     if (r >= n) return;
     const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
     if (pi.y == 0) return;
     RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
     gen.init(src.load(r), s);
-    if (resume) gen.resume(s, resume[r]);
     LaneWriter<SCH, VEC> w;
     w.start((int32_t)(ray_index_base + r), pi.x, pi.y);
     Run run;
@@ -430,150 +471,83 @@ __global__ void __launch_bounds__(kWriteBlock)
     w.flush(o, s);
 }
 
-// ---------------------------------------------------------------------------
-// Persistent-thread variants (the default launch path).  One analyzer event
-// per loop iteration and per lane; a lane that finishes its ray immediately
-// takes the next ray id from its warp's batch, so warps stay full no matter
-// how unevenly the work is spread over rays (0..200 samples, 10..300 events).
-// Batches of 32 consecutive ray ids keep neighbouring (coherent) rays in one
-// warp; the next batch is prefetched with one atomic so that the refill never
-// waits on it.
-// ---------------------------------------------------------------------------
-constexpr int kPBlock = 128;
+// pass 2: slabs -> packed arrays.  A block owns kGather consecutive rays, whose samples
+// form one contiguous output range; thread i handles output samples i, i + kGather, ...
+// (consecutive threads on consecutive samples: every store is coalesced and every output
+// sector is written whole by one warp).  The owning ray of a sample is a binary search
+// over the block's offsets in shared memory.  Samples past a ray's slab are tail_kernel's.
+constexpr int kGather = 256;
 
-struct RayDispenser {
-    unsigned long long* ctr;
-    long long cur_base;
-    int cur_used;
-    unsigned long long pf; // lane 0: prefetched next batch base
-
-    __device__ __forceinline__ void init(unsigned long long* c, int lane) {
-        ctr = c;
-        unsigned long long b = 0;
-        if (lane == 0) {
-            b = atomicAdd(ctr, 32ull);
-            pf = atomicAdd(ctr, 32ull);
-        }
-        cur_base = (long long)__shfl_sync(0xffffffffu, b, 0);
-        cur_used = 0;
+template <int SCH>
+__global__ void __launch_bounds__(kGather)
+    gather_kernel(const SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
+                  const SlabDev S, int64_t ray_index_base, const Out o) {
+    __shared__ long long s_base[2];
+    __shared__ int s_off[kGather]; // ray offsets relative to the block's first sample
+    __shared__ int s_fill[kGather];
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * kGather;
+    const int nr = (int)(n - r0 < kGather ? n - r0 : kGather);
+    const int64_t r = r0 + tid;
+    longlong2 pi = make_longlong2(0, 0);
+    if (tid < nr) pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
+    if (tid == 0) s_base[0] = pi.x;
+    if (tid == nr - 1) s_base[1] = pi.x + pi.y;
+    __syncthreads();
+    const long long O0 = s_base[0], O1 = s_base[1];
+    // a block's samples (<= kGather * max per-ray count) fit 31 bits
+    s_off[tid] = tid < nr ? (int)(pi.x - O0) : INT_MAX;
+    int fill = (int)(pi.y < S.C ? pi.y : S.C);
+    if (tid < nr && pi.y > S.C) fill = S.resume[r].tag >> 8; // overflowed: what pass 1 put in the slab
+    s_fill[tid] = fill;
+    __syncthreads();
+    const int m = (int)(O1 - O0);
+    for (int e = tid; e < m; e += kGather) {
+        int j = 0; // largest j with s_off[j] <= e: branch-free binary search over 256 entries
+#pragma unroll
+        for (int step = kGather / 2; step > 0; step >>= 1)
+            j += (s_off[j + step] <= e) ? step : 0;
+        const int k = e - s_off[j];
+        if (k >= s_fill[j]) continue;
+        const int64_t i = (r0 + j) * S.C + k;
+        const long long g = O0 + e;
+        const double t = __ldcs(S.t + i);
+        __stcs(o.t_starts + g, t);
+        if (o.t_ends) __stcs(o.t_ends + g, t + ladder_step<SCH>(t, s.dt0, s.growth));
+        if (o.ray_indices) __stcs(o.ray_indices + g, (int32_t)(ray_index_base + r0 + j));
+        if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, __ldcs(reinterpret_cast<const unsigned int*>(S.cell) + i));
+        if (o.levels) o.levels[g] = S.lvl[i];
     }
-    // ray id for this lane if it is in `need` (warp-uniform call)
-    __device__ __forceinline__ long long take(unsigned need, int lane) {
-        const int k = __popc(need);
-        const int rank = __popc(need & ((1u << lane) - 1u));
-        const int avail = 32 - cur_used;
-        long long id;
-        if (k <= avail) {
-            id = cur_base + cur_used + rank;
-            cur_used += k;
-        } else {
-            const long long nb = (long long)__shfl_sync(0xffffffffu, pf, 0);
-            id = rank < avail ? cur_base + cur_used + rank : nb + (rank - avail);
-            cur_base = nb;
-            cur_used = k - avail;
-            if (lane == 0) pf = atomicAdd(ctr, 32ull);
-        }
-        return id;
-    }
-};
-
-template <int AN, bool CASC, bool BR, int SCH, class Src>
-__global__ void __launch_bounds__(kPBlock)
-    count_persistent(const SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
-                     int64_t* __restrict__ stats, uint8_t* __restrict__ status,
-                     int32_t* __restrict__ counters, Resume* __restrict__ resume,
-                     unsigned long long* __restrict__ ray_ctr) {
-    const int lane = threadIdx.x & 31;
-    RayDispenser disp;
-    disp.init(ray_ctr, lane);
-    RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
-    bool have = false, exhausted = false;
-    long long r = 0, cnt = 0;
-    Stats5 acc;
-    for (;;) {
-        const unsigned need = __ballot_sync(0xffffffffu, !have);
-        bool got = false;
-        // refill idle lanes once enough are idle (or the warp has nothing to do)
-        if (!exhausted && need && (__popc(need) >= s.refill_min || need == 0xffffffffu)) {
-            const long long id = disp.take(need, lane);
-            if (!have && id < n) {
-                got = true;
-                r = id;
-                const Ray ray = src.load(r);
-                if (!ray_valid(ray)) {
-                    count_invalid(r, packed, status, counters, acc);
-                } else {
-                    gen.init(ray, s);
-                    have = true;
-                    cnt = 0;
-                }
-            }
-            exhausted = __any_sync(0xffffffffu, !have && !got && ((need >> lane) & 1u));
-        }
-        if (!__any_sync(0xffffffffu, have)) {
-            if (!exhausted) continue;
-            break;
-        }
-        if (have) {
-            Run run;
-            const int st = gen.step(s, run);
-            if (st == 2) {
-                if (cnt == 0 && resume) store_resume(resume + r, run);
-                cnt += run.n;
-            } else if (st == 0) {
-                count_finish(gen, r, cnt, packed, status, counters, acc);
-                have = false;
-            }
-        }
-    }
-    acc.flush(stats);
 }
 
+// pass 2 for the rays whose slab overflowed: resume the traversal at the first run that
+// did not fit and write the rest of the ray directly
 template <int AN, bool CASC, bool BR, int SCH, bool VEC, class Src>
-__global__ void __launch_bounds__(kPBlock)
-    write_persistent(const SamplerDev s, const Src src, int64_t n, const int64_t* __restrict__ packed,
-                     const Resume* __restrict__ resume, int64_t ray_index_base, const Out o,
-                     unsigned long long* __restrict__ ray_ctr) {
-    const int lane = threadIdx.x & 31;
-    RayDispenser disp;
-    disp.init(ray_ctr, lane);
-    RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
-    LaneWriter<SCH, VEC> w;
-    bool have = false, exhausted = false;
-    for (;;) {
-        const unsigned need = __ballot_sync(0xffffffffu, !have);
-        bool got = false;
-        if (!exhausted && need && (__popc(need) >= s.refill_min || need == 0xffffffffu)) {
-            const long long id = disp.take(need, lane);
-            if (!have && id < n) {
-                got = true;
-                const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + id);
-                if (pi.y > 0) {
-                    gen.init(src.load(id), s);
-                    if (resume) gen.resume(s, resume[id]);
-                    w.start((int32_t)(ray_index_base + id), pi.x, pi.y);
-                    have = true;
-                }
-            }
-            exhausted = __any_sync(0xffffffffu, !have && !got && ((need >> lane) & 1u));
-        }
-        if (!__any_sync(0xffffffffu, have)) {
-            if (!exhausted) continue;
-            break;
-        }
-        if (have) {
+__global__ void __launch_bounds__(kWriteBlock)
+    tail_kernel(const SamplerDev s, const Src src, const int64_t* __restrict__ packed,
+                const SlabDev S, int64_t ray_index_base, const Out o) {
+    const unsigned cnt = *S.ovf_ctr;
+    for (unsigned i = blockIdx.x * kWriteBlock + threadIdx.x; i < cnt; i += gridDim.x * kWriteBlock) {
+        const int64_t r = S.ovf_list[i];
+        const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
+        Resume res = S.resume[r];
+        const long long skip = res.tag >> 8;
+        res.tag &= 255;
+        RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
+        gen.init(src.load(r), s);
+        gen.resume(s, res);
+        LaneWriter<SCH, VEC> w;
+        w.start((int32_t)(ray_index_base + r), pi.x + skip, pi.y - skip);
+        Run run;
+        while (!w.done()) {
             if (w.prem == 0) {
-                Run run;
                 const int st = gen.step(s, run);
+                if (st == 0) break;
                 if (st == 2) w.take(run);
-                else if (st == 0) w.end = w.out + w.nb; // unreachable when passes agree
             }
             w.emit4(o, s);
-            if (w.done()) {
-                w.flush(o, s);
-                have = false;
-            }
         }
+        w.flush(o, s);
     }
 }
 
@@ -588,11 +562,19 @@ __global__ void raygen_kernel(const CameraDev cam, int64_t first, int64_t n, dou
     p[3] = make_double2(r.tmin, r.tmax);
 }
 
+
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
-// resident blocks per SM x SMs (cached per kernel), capped by the work available
-static unsigned persistent_grid(const void* kernel, int64_t n) {
+static bool vec_ok(const Out& o) { // 256-bit stores need 32-byte aligned bases (16 for 4-byte arrays)
+    return (reinterpret_cast<uintptr_t>(o.t_starts) & 31) == 0 &&
+           (reinterpret_cast<uintptr_t>(o.t_ends) & 31) == 0 &&
+           (reinterpret_cast<uintptr_t>(o.ray_indices) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(o.cells) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(o.levels) & 3) == 0;
+}
+
+static unsigned tail_grid(int64_t n) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -600,72 +582,41 @@ static unsigned persistent_grid(const void* kernel, int64_t n) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
     }
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kPBlock, 0) != cudaSuccess || per_sm <= 0)
-        per_sm = 4;
-    const int64_t want = (n + 31) / 32 / (kPBlock / 32) + 1;
-    int64_t g = (int64_t)sms * per_sm;
-    if (g > want) g = want;
-    return (unsigned)(g < 1 ? 1 : g);
+    const int64_t want = (n + kWriteBlock - 1) / kWriteBlock;
+    const int64_t cap = (int64_t)sms * 8;
+    return (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
 }
 
 template <class Src>
 struct Launch {
     template <int AN, bool CASC, bool BR, int SCH>
     static cudaError_t count(const SamplerDev& s, const Src& src, int64_t n, int64_t* packed,
-                             int64_t* stats, uint8_t* status, int32_t* counters, Resume* resume,
+                             int64_t* stats, uint8_t* status, int32_t* counters, const SlabDev& S,
                              cudaStream_t st) {
         const int64_t blocks = (n + kBlock - 1) / kBlock;
         count_kernel<AN, CASC, BR, SCH, Src>
-            <<<(unsigned)blocks, kBlock, 0, st>>>(s, src, n, packed, stats, status, counters, resume);
-        return cudaGetLastError();
-    }
-    template <int AN, bool CASC, bool BR, int SCH>
-    static cudaError_t count_p(const SamplerDev& s, const Src& src, int64_t n, int64_t* packed,
-                               int64_t* stats, uint8_t* status, int32_t* counters, Resume* resume,
-                               unsigned long long* ctr, cudaStream_t st) {
-        auto k = count_persistent<AN, CASC, BR, SCH, Src>;
-        const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), n);
-        k<<<grid, kPBlock, 0, st>>>(s, src, n, packed, stats, status, counters, resume, ctr);
-        return cudaGetLastError();
-    }
-    template <int AN, bool CASC, bool BR, int SCH>
-    static cudaError_t write_p(const SamplerDev& s, const Src& src, int64_t n, const int64_t* packed,
-                               const Resume* resume, int64_t base, double* ts, double* te, int32_t* ri,
-                               uint32_t* ce, uint8_t* lv, unsigned long long* ctr, cudaStream_t st) {
-        const Out o{ts, te, ri, ce, lv};
-        const bool vec = (reinterpret_cast<uintptr_t>(ts) & 31) == 0 &&
-                         (reinterpret_cast<uintptr_t>(te) & 31) == 0 &&
-                         (reinterpret_cast<uintptr_t>(ri) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(ce) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(lv) & 3) == 0;
-        if (vec) {
-            auto k = write_persistent<AN, CASC, BR, SCH, true, Src>;
-            k<<<persistent_grid(reinterpret_cast<const void*>(k), n), kPBlock, 0, st>>>(s, src, n, packed, resume, base, o, ctr);
-        } else {
-            auto k = write_persistent<AN, CASC, BR, SCH, false, Src>;
-            k<<<persistent_grid(reinterpret_cast<const void*>(k), n), kPBlock, 0, st>>>(s, src, n, packed, resume, base, o, ctr);
-        }
+            <<<(unsigned)blocks, kBlock, 0, st>>>(s, src, n, packed, stats, status, counters, S);
         return cudaGetLastError();
     }
     template <int AN, bool CASC, bool BR, int SCH>
     static cudaError_t write(const SamplerDev& s, const Src& src, int64_t n, const int64_t* packed,
-                             const Resume* resume, int64_t base, double* ts, double* te, int32_t* ri,
-                             uint32_t* ce, uint8_t* lv, cudaStream_t st) {
-        const int64_t blocks = (n + kWriteBlock - 1) / kWriteBlock;
-        const Out o{ts, te, ri, ce, lv};
-        // 256-bit stores need 32-byte aligned bases (16 for the 4-byte arrays)
-        const bool vec = (reinterpret_cast<uintptr_t>(ts) & 31) == 0 &&
-                         (reinterpret_cast<uintptr_t>(te) & 31) == 0 &&
-                         (reinterpret_cast<uintptr_t>(ri) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(ce) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(lv) & 3) == 0;
+                             const SlabDev* S, int64_t base, const Out& o, cudaStream_t st) {
+        const unsigned blocks = (unsigned)((n + kWriteBlock - 1) / kWriteBlock);
+        const bool vec = vec_ok(o);
+        if (!S) {
+            if (vec)
+                write_kernel<AN, CASC, BR, SCH, true, Src><<<blocks, kWriteBlock, 0, st>>>(s, src, n, packed, base, o);
+            else
+                write_kernel<AN, CASC, BR, SCH, false, Src><<<blocks, kWriteBlock, 0, st>>>(s, src, n, packed, base, o);
+            return cudaGetLastError();
+        }
+        const unsigned gb = (unsigned)((n + kGather - 1) / kGather);
+        gather_kernel<SCH><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
+        const unsigned tg = tail_grid(n);
         if (vec)
-            write_kernel<AN, CASC, BR, SCH, true, Src>
-                <<<(unsigned)blocks, kWriteBlock, 0, st>>>(s, src, n, packed, resume, base, o);
+            tail_kernel<AN, CASC, BR, SCH, true, Src><<<tg, kWriteBlock, 0, st>>>(s, src, packed, *S, base, o);
         else
-            write_kernel<AN, CASC, BR, SCH, false, Src>
-                <<<(unsigned)blocks, kWriteBlock, 0, st>>>(s, src, n, packed, resume, base, o);
+            tail_kernel<AN, CASC, BR, SCH, false, Src><<<tg, kWriteBlock, 0, st>>>(s, src, packed, *S, base, o);
         return cudaGetLastError();
     }
 };
@@ -696,19 +647,16 @@ struct Launch {
 // Variant key: analyzer (0 dda / 1 hdda), cascade, kernel == branch, schedule == linear.
 cudaError_t launch_count(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, int64_t* packed,
-                         int64_t* stats, uint8_t* status, int32_t* counters, void* resume,
-                         unsigned long long* ctr, cudaStream_t st) {
-    Resume* res = static_cast<Resume*>(resume);
+                         int64_t* stats, uint8_t* status, int32_t* counters, const SlabDev& slab,
+                         cudaStream_t st) {
     if (cam) {
         using L = Launch<RaysFromCamera>;
         const RaysFromCamera src{*cam, first};
-        if (ctr) SOGK_DISPATCH(count_p, s, src, n, packed, stats, status, counters, res, ctr, st);
-        SOGK_DISPATCH(count, s, src, n, packed, stats, status, counters, res, st);
+        SOGK_DISPATCH(count, s, src, n, packed, stats, status, counters, slab, st);
     } else {
         using L = Launch<RaysFromBuffer>;
         const RaysFromBuffer src{rays};
-        if (ctr) SOGK_DISPATCH(count_p, s, src, n, packed, stats, status, counters, res, ctr, st);
-        SOGK_DISPATCH(count, s, src, n, packed, stats, status, counters, res, st);
+        SOGK_DISPATCH(count, s, src, n, packed, stats, status, counters, slab, st);
     }
 }
 
@@ -724,19 +672,17 @@ size_t resume_bytes(int64_t n) { return size_t(n) * sizeof(Resume); }
 
 cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, const int64_t* packed,
-                         const void* resume, int64_t base, double* ts, double* te, int32_t* ri,
-                         uint32_t* ce, uint8_t* lv, unsigned long long* ctr, cudaStream_t st) {
-    const Resume* res = static_cast<const Resume*>(resume);
+                         const SlabDev* slab, int64_t base, double* ts, double* te, int32_t* ri,
+                         uint32_t* ce, uint8_t* lv, cudaStream_t st) {
+    const Out o{ts, te, ri, ce, lv};
     if (cam) {
         using L = Launch<RaysFromCamera>;
         const RaysFromCamera src{*cam, first};
-        if (ctr) SOGK_DISPATCH(write_p, s, src, n, packed, res, base, ts, te, ri, ce, lv, ctr, st);
-        SOGK_DISPATCH(write, s, src, n, packed, res, base, ts, te, ri, ce, lv, st);
+        SOGK_DISPATCH(write, s, src, n, packed, slab, base, o, st);
     } else {
         using L = Launch<RaysFromBuffer>;
         const RaysFromBuffer src{rays};
-        if (ctr) SOGK_DISPATCH(write_p, s, src, n, packed, res, base, ts, te, ri, ce, lv, ctr, st);
-        SOGK_DISPATCH(write, s, src, n, packed, res, base, ts, te, ri, ce, lv, st);
+        SOGK_DISPATCH(write, s, src, n, packed, slab, base, o, st);
     }
 }
 

@@ -28,4 +28,4 @@ for it in range(2):
     tot = int(stats[0].item())
     s.write(rays, packed, tot, levels=False)
 torch.cuda.synchronize()
-print("total samples", tot)
+print("total samples", tot, "stats", stats.cpu().tolist())
