@@ -793,7 +793,7 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     s->v.cascade = cascade ? 1 : 0;
     s->v.branch = desc->kernel == SOGK_BRANCH ? 1 : 0;
     s->v.linear = desc->schedule == SOGK_LINEAR ? 1 : 0;
-    if (const char* e = std::getenv("SOGK_SLAB")) s->slab_cap = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("SOGK_SLAB")) s->slab_cap = (std::max(0, std::atoi(e)) + 3) & ~3; // multiple of 4
     for (int b = 0; b < n_levels; ++b) s->dev.lv[b] = levels[b]->dev();
     s->dev.n_levels = n_levels;
     s->dev.spin_cap = desc->spin_cap > 0 ? desc->spin_cap : SOGK_DEFAULT_SPIN_CAP;

@@ -177,9 +177,11 @@ __device__ __forceinline__ bool dense_voxel(const GridDev& g, const int ijk[3]) 
 // over the GPU layout of sogk_layout.h.  The per-thread leaf cache plays the
 // role of the reference Accessor's cached leaf; answers are identical.
 // ---------------------------------------------------------------------------
+// A query answer.  Every node the reference returns is aligned to its extent
+// (region_origin = floor_div(ijk, 128) * 128, tile/leaf origins ijk & ~7, voxels ijk),
+// so the origin is always ijk & -extent and is not carried.
 struct Query {
-    int origin[3];
-    int extent;
+    int ext;   // 1, 8 or 128
     int level;
     bool occ;
 };
@@ -200,19 +202,13 @@ struct VdbCursor {
             const uint64_t w = __ldg(g.leaves + leaf * 8 + lz);
             q.occ = (w >> ((ly << 3) | lx)) & 1ull;
             q.level = LV_VOXEL;
-            q.extent = 1;
-            q.origin[0] = ijk[0];
-            q.origin[1] = ijk[1];
-            q.origin[2] = ijk[2];
+            q.ext = 1;
             return q;
         }
         q.occ = false;
         q.level = LV_ROOT_TILE;
-        q.extent = 128;
-        q.origin[0] = (ijk[0] >> 7) << 7; // region_origin = floor_div(ijk, 128) * 128 (:159)
-        q.origin[1] = (ijk[1] >> 7) << 7;
-        q.origin[2] = (ijk[2] >> 7) << 7;
-        if (!in_bounds(g, ijk)) return q; // background root tile (:164-165)
+        q.ext = 128;
+        if (!in_bounds(g, ijk)) return q; // background root tile at region_origin (:164-165)
         const int region = ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7);
         const int32_t node = __ldg(g.root + region);
         q.level = LV_INTERNAL_TILE;
@@ -224,26 +220,20 @@ struct VdbCursor {
         const int64_t wi = (int64_t)node * 64 + (ci >> 6);
         const uint64_t cm = __ldg(g.child_mask + wi);
         const int b = ci & 63;
-        q.origin[0] = ijk[0] & ~7;
-        q.origin[1] = ijk[1] & ~7;
-        q.origin[2] = ijk[2] & ~7;
         if (!((cm >> b) & 1ull)) { // tile child (:205-208)
             q.occ = (__ldg(g.value_mask + wi) >> b) & 1ull;
             q.level = LV_LEAF_TILE;
-            q.extent = 8;
+            q.ext = 8;
             return q;
         }
         leaf = (int64_t)__ldg(g.prefix + wi) + __popcll(cm & ((1ull << b) - 1ull));
-        lo[0] = q.origin[0];
-        lo[1] = q.origin[1];
-        lo[2] = q.origin[2];
+        lo[0] = ijk[0] & ~7;
+        lo[1] = ijk[1] & ~7;
+        lo[2] = ijk[2] & ~7;
         const uint64_t w = __ldg(g.leaves + leaf * 8 + (ijk[2] & 7));
         q.occ = (w >> (((ijk[1] & 7) << 3) | (ijk[0] & 7))) & 1ull;
         q.level = LV_VOXEL;
-        q.extent = 1;
-        q.origin[0] = ijk[0];
-        q.origin[1] = ijk[1];
-        q.origin[2] = ijk[2];
+        q.ext = 1;
         return q;
     }
 };
@@ -357,6 +347,10 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
         return dense_voxel(g, ev.ijk);
     }
 
+    __device__ __forceinline__ bool is_valid() const { return geom.valid; }
+    __device__ __forceinline__ double enter_t() const { return geom.t_enter; }
+    __device__ __forceinline__ double exit_t() const { return geom.t_exit; }
+
     // Resume at an emitted event: (ijk, t_cur) = (ev.ijk, ev.t0) reproduces it.
     __device__ __forceinline__ void restore(const GridDev& g, const int in_ijk[3], double in_t) {
         done = false;
@@ -371,9 +365,25 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
     }
 };
 
-struct HddaAn { // HddaTraversal, traversal.hpp:199-264
+// HddaTraversal, traversal.hpp:199-264.
+//
+// The loop runs in per-axis mirrored coordinates: an axis the ray walks down is
+// negated (entry' = -entry, dir' = -dir, inv' = -inv, plane' = -plane), so every
+// moving axis walks up.  Negation is exact and round-to-nearest is symmetric, so
+//   plane_t:    t_enter + (plane' - entry') * inv'  ==  t_enter + (plane - entry) * inv
+//   grid_coord: entry' + dt * dir'                  == -(entry + dt * dir)
+// bit for bit, and cell_after_crossing's "floor, minus one on an exact plane
+// when walking down" (traversal.hpp:96-100) becomes ~floor(grid_coord') there:
+//   ceil(x) - 1 == -floor(-x) - 1 == ~floor(-x).
+// A static axis (dir == 0) gets entry' = cell + 0.5, dir' = 0, inv' = +inf: its
+// exit time is +inf (the reference's kInfiniteStep: only ever compared, never the
+// minimum of a valid ray) and its re-derived cell is its constant cell.
+struct HddaAn {
     static constexpr bool kHdda = true;
-    Geom geom;
+    double e[3], dv[3], iv[3]; // mirrored entry, |dir|, 1/|dir|
+    int m[3];                  // -1 on mirrored axes, else 0
+    double t_enter, t_exit;
+    bool valid;
     int ijk[3];
     double t_cur;
     int lookups, steps;
@@ -389,75 +399,88 @@ struct HddaAn { // HddaTraversal, traversal.hpp:199-264
         spin_cap = cap;
         degenerate = 0;
         cur.reset();
+        Geom geom;
         geom.init(r, g);
-        done = !geom.valid;
+        valid = geom.valid;
+        t_enter = geom.t_enter;
+        t_exit = geom.t_exit;
+        done = !valid;
         if (done) return;
         geom.entry_cell(g.res, ijk);
         t_cur = geom.t_enter;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (geom.step[a] > 0) {
+                e[a] = geom.entry[a];
+                dv[a] = geom.dir[a];
+                iv[a] = geom.inv[a];
+                m[a] = 0;
+            } else if (geom.step[a] < 0) {
+                e[a] = -geom.entry[a];
+                dv[a] = -geom.dir[a];
+                iv[a] = -geom.inv[a];
+                m[a] = -1;
+            } else {
+                e[a] = (double)ijk[a] + 0.5;
+                dv[a] = 0.0;
+                iv[a] = __longlong_as_double(0x7ff0000000000000ll); // +inf
+                m[a] = 0;
+            }
+        }
     }
 
     // One iteration of HddaTraversal::next's loop (:213-248): 1 = event, 0 = end,
     // -1 = degenerate iteration consumed (call again).
     __device__ __forceinline__ int next(const GridDev& g, Event& ev) {
         if (done) return 0;
-        {
-            const Query q = cur.query(g, ijk);
-            ++lookups;
-            // exit plane of the node on each moving axis (:218-228), and the cell
-            // just past it (`stepped`, :236-237)
-            double tc[3];
-            int stepped[3];
+        const Query q = cur.query(g, ijk);
+        ++lookups;
+        // exit plane of the node on each axis (:218-228), mirrored: lo + ext walking up,
+        // -lo walking down; the cell just past it (`stepped`, :236-237) is plane' ^ m
+        double tc[3];
+        int pl[3];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const int hi = q.origin[a] + q.extent;
-                const int plane = geom.step[a] > 0 ? hi : q.origin[a];
-                stepped[a] = geom.step[a] > 0 ? hi : q.origin[a] - 1;
-                const double pt = geom.plane_t(a, (double)plane);
-                tc[a] = geom.step[a] == 0 ? kInf : pt;
-            }
-            double t1;
-            const int axis = argmin3(tc[0], tc[1], tc[2], t1);
-            ev.ijk[0] = q.origin[0];
-            ev.ijk[1] = q.origin[1];
-            ev.ijk[2] = q.origin[2];
-            ev.level = q.level;
-            ev.occ = q.occ;
-            if (t1 >= geom.t_exit) {
-                ++steps;
-                done = true;
-                ev.t0 = t_cur;
-                ev.t1 = geom.t_exit;
-                return 1;
-            }
-            const bool degen = t1 <= t_cur; // degenerate corner crossing (:238-241)
-            // cell_after_crossing (:91-104) at t_cur (degenerate) or t1, all axes
-            // evaluated and the stepped one overridden: no data-dependent branch
-            const double tt = degen ? t_cur : t1;
-            const double dt = tt - geom.t_enter;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const double gc = geom.entry[a] + dt * geom.dir[a];
-                double c = floor(gc);
-                if (geom.step[a] < 0 && c == gc) c -= 1.0;
-                const int moved = geom.step[a] != 0 ? (int)c : ijk[a];
-                ijk[a] = (a == axis) ? stepped[a] : moved;
-            }
-            if (degen) {
-                // the reference spins forever at exact edge crossings
-                if (++degenerate > spin_cap) {
-                    undefined = true;
-                    done = true;
-                    return 0;
-                }
-                return -1;
-            }
-            degenerate = 0;
-            ev.t0 = t_cur;
-            ev.t1 = t1;
+        for (int a = 0; a < 3; ++a) {
+            const int lo = ijk[a] & -q.ext;
+            ev.ijk[a] = lo;
+            pl[a] = (lo ^ m[a]) + (m[a] ? 1 : q.ext);
+            tc[a] = t_enter + ((double)pl[a] - e[a]) * iv[a];
+        }
+        double t1;
+        const int axis = argmin3(tc[0], tc[1], tc[2], t1);
+        ev.level = q.level;
+        ev.occ = q.occ;
+        if (t1 >= t_exit) {
             ++steps;
-            t_cur = t1;
+            done = true;
+            ev.t0 = t_cur;
+            ev.t1 = t_exit;
             return 1;
         }
+        const bool degen = t1 <= t_cur; // degenerate corner crossing (:238-241)
+        // cell_after_crossing (:91-104) at t_cur (degenerate) or t1, all axes
+        // evaluated and the stepped one overridden
+        const double dt = (degen ? t_cur : t1) - t_enter;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int c = __double2int_rd(e[a] + dt * dv[a]) ^ m[a];
+            ijk[a] = (a == axis) ? (pl[a] ^ m[a]) : c;
+        }
+        if (degen) {
+            // the reference spins forever at exact edge crossings
+            if (++degenerate > spin_cap) {
+                undefined = true;
+                done = true;
+                return 0;
+            }
+            return -1;
+        }
+        degenerate = 0;
+        ev.t0 = t_cur;
+        ev.t1 = t1;
+        ++steps;
+        t_cur = t1;
+        return 1;
     }
 
     __device__ __forceinline__ bool probe(const GridDev& g, const Event& ev) { // SparseProbe
@@ -475,6 +498,10 @@ struct HddaAn { // HddaTraversal, traversal.hpp:199-264
         ijk[2] = in_ijk[2];
         cur.reset(); // the accessor cache is semantically transparent
     }
+
+    __device__ __forceinline__ bool is_valid() const { return valid; }
+    __device__ __forceinline__ double enter_t() const { return t_enter; }
+    __device__ __forceinline__ double exit_t() const { return t_exit; }
 };
 
 // CascadeTraversal<GridT>, sampling.hpp:305-415, over SOGK_MAX_LEVELS levels
@@ -631,9 +658,9 @@ struct AnyAn<Sub, false> {
     __device__ __forceinline__ void init(const Ray& r, const SamplerDev& s) {
         an.init(r, s.lv[0], s.spin_cap);
     }
-    __device__ __forceinline__ bool valid() const { return an.geom.valid; }
-    __device__ __forceinline__ double t_enter() const { return an.geom.t_enter; }
-    __device__ __forceinline__ double t_exit() const { return an.geom.t_exit; }
+    __device__ __forceinline__ bool valid() const { return an.is_valid(); }
+    __device__ __forceinline__ double t_enter() const { return an.enter_t(); }
+    __device__ __forceinline__ double t_exit() const { return an.exit_t(); }
     __device__ __forceinline__ int next(const SamplerDev& s, Event& ev) {
         const int r = an.next(s.lv[0], ev);
         ev.grid_level = 0;
