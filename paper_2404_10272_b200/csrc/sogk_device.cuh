@@ -741,14 +741,18 @@ struct RunGen {
         t_end = an.t_exit();
     }
 
-    // One analyzer call (one event):
-    // 0 = ray finished, 1 = event without samples, 2 = `run` holds the event's samples.
-    __device__ __forceinline__ int step(const SamplerDev& s, Run& run) {
+    // One analyzer call (one event) for callers that emit the samples themselves:
+    // 0 = ray finished, 1 = nothing to emit, 2 = occupied event `ev`: the ladder has been
+    // advanced past ev.t0 (t_last0 = where it stood before) and the caller takes the
+    // points t_last <= ev.t1 (sampling.hpp:96-99, 115-118), e.g. with seek_to().
+    // The branch kernel's per-point probe (DenseProbe / SparseProbe / CascadeProbe) asks
+    // the grid about ev.ijk, i.e. the event's own cell or node, so it always answers
+    // ev.occ; it is not evaluated, only counted (kernel_lookups += points of the event).
+    __device__ __forceinline__ int step_event(const SamplerDev& s, Event& ev, double& t_last0) {
         if (!(alive && t_last <= t_end)) {
             alive = false;
             return 0;
         }
-        Event ev;
         const int got = an.next(s, ev);
         if (got == 0) {
             alive = false;
@@ -756,33 +760,51 @@ struct RunGen {
         }
         if (got < 0) return 1; // analyzer-internal iteration, no event yet
         if (!Branch && !ev.occ) return 1;
-        const double t_last0 = t_last;
+        t_last0 = t_last;
         ladder_seek<Sched>(t_last, ev.t0, s.dt0, s.inv_dt0, s.growth, s.t_switch, stalled);
-        const double first = t_last;
-        const int n = (int)ladder_seek<Sched>(t_last, ev.t1, s.dt0, s.inv_dt0, s.growth, s.t_switch, stalled);
+        if (!ev.occ) { // branch kernel, empty event: its points are probed, not sampled
+            kernel_lookups += (int)ladder_seek<Sched>(t_last, ev.t1, s.dt0, s.inv_dt0, s.growth,
+                                                      s.t_switch, stalled);
+            if (stalled) alive = false;
+            return stalled ? 0 : 1;
+        }
         if (stalled) {
             alive = false;
             return 0;
         }
-        bool occ = ev.occ;
-        if (Branch) {
-            kernel_lookups += n;
-            if (n > 0) occ = an.probe(s, ev);
-        }
-        if (n > 0 && occ) {
-            run.first = first;
-            run.n = n;
-            run.cell = pack_cell(ev.ijk);
-            run.level = (uint8_t)(ev.level | (ev.grid_level << 2));
-            run.ijk[0] = ev.ijk[0];
-            run.ijk[1] = ev.ijk[1];
-            run.ijk[2] = ev.ijk[2];
-            run.tag = an.resume_tag();
-            run.t0 = ev.t0;
-            run.t_last0 = t_last0;
-            return 2;
-        }
-        return 1;
+        return 2;
+    }
+
+    // take the remaining points <= T in closed form; returns how many
+    __device__ __forceinline__ int seek_to(const SamplerDev& s, double T) {
+        const int n = (int)ladder_seek<Sched>(t_last, T, s.dt0, s.inv_dt0, s.growth, s.t_switch, stalled);
+        if (stalled) alive = false;
+        return n;
+    }
+
+    // One analyzer call (one event):
+    // 0 = ray finished, 1 = event without samples, 2 = `run` holds the event's samples.
+    __device__ __forceinline__ int step(const SamplerDev& s, Run& run) {
+        Event ev;
+        double t_last0;
+        const int st = step_event(s, ev, t_last0);
+        if (st != 2) return st;
+        const double first = t_last;
+        const int n = seek_to(s, ev.t1);
+        if (stalled) return 0;
+        if (Branch) kernel_lookups += n;
+        if (n == 0) return 1;
+        run.first = first;
+        run.n = n;
+        run.cell = pack_cell(ev.ijk);
+        run.level = (uint8_t)(ev.level | (ev.grid_level << 2));
+        run.ijk[0] = ev.ijk[0];
+        run.ijk[1] = ev.ijk[1];
+        run.ijk[2] = ev.ijk[2];
+        run.tag = an.resume_tag();
+        run.t0 = ev.t0;
+        run.t_last0 = t_last0;
+        return 2;
     }
 
     // next run with n >= 1 samples; false at the end of the ray

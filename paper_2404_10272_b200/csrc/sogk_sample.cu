@@ -227,36 +227,50 @@ __global__ void __launch_bounds__(kBlock, SOGK_COUNT_MINB)
         } else {
             RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
             gen.init(ray, s);
+            const int64_t row = r * S.C;
             long long c = 0;
             int filled = 0;     // samples in the slab
-            bool ovf = S.C == 0; // slab closed: the rest comes from the resume state
+            bool ovf = false;   // slab full: the rest of the ray comes from its resume state
             bool stored = false;
-            Run run;
             for (;;) { // one flat loop: one analyzer step per iteration
-                const int st = gen.step(s, run);
+                Event ev;
+                double t_last0;
+                const int st = gen.step_event(s, ev, t_last0);
                 if (st == 0) break;
-                if (st == 2) {
-                    if (!ovf) {
-                        if (filled + run.n <= S.C) {
-                            const int64_t base = r * S.C + filled;
-                            double t = run.first;
-                            for (int i = 0; i < run.n; ++i) {
-                                S.t[base + i] = t;
-                                S.cell[base + i] = run.cell;
-                                S.lvl[base + i] = run.level;
-                                t = t + ladder_step<SCH>(t, s.dt0, s.growth);
-                            }
-                            filled += run.n;
-                        } else {
-                            ovf = true;
-                        }
+                if (st == 1) continue;
+                int k = 0; // points of this event
+                if (!ovf) { // the reference loop itself: while (t <= t1) { push(t); t += step(t); }
+                    const uint32_t cell = pack_cell(ev.ijk);
+                    const uint8_t lvl = (uint8_t)(ev.level | (ev.grid_level << 2));
+                    double t = gen.t_last;
+                    const int64_t base = row + filled;
+                    const int room = (int)S.C - filled;
+                    while (t <= ev.t1 && k < room) {
+                        S.t[base + k] = t;
+                        S.cell[base + k] = cell;
+                        S.lvl[base + k] = lvl;
+                        t = t + ladder_step<SCH>(t, s.dt0, s.growth);
+                        ++k;
                     }
-                    if (ovf && !stored) {
+                    gen.t_last = t;
+                    if (t <= ev.t1) { // slab full inside this event: it restarts in tail_kernel
+                        ovf = true;
+                        Run run;
+                        run.ijk[0] = ev.ijk[0];
+                        run.ijk[1] = ev.ijk[1];
+                        run.ijk[2] = ev.ijk[2];
+                        run.tag = gen.an.resume_tag();
+                        run.t0 = ev.t0;
+                        run.t_last0 = t_last0;
                         store_resume(S.resume + r, run, filled);
                         stored = true;
+                    } else {
+                        filled += k;
                     }
-                    c += run.n;
                 }
+                if (ovf) k += gen.seek_to(s, ev.t1); // counted, not stored
+                if (BR) gen.kernel_lookups += k;
+                c += k;
             }
             count_finish(gen, r, c, packed, status, counters, acc);
             if (stored && c > 0 && !gen.undefined()) {
