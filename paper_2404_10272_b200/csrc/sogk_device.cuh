@@ -378,11 +378,49 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
 // A static axis (dir == 0) gets entry' = cell + 0.5, dir' = 0, inv' = +inf: its
 // exit time is +inf (the reference's kInfiniteStep: only ever compared, never the
 // minimum of a valid ray) and its re-derived cell is its constant cell.
+#ifndef SOGK_HDDA_SMEM
+#define SOGK_HDDA_SMEM 1
+#endif
+#if SOGK_HDDA_SMEM
+// The per-ray geometry lives in shared memory (one column per thread, SoA: conflict-free),
+// which keeps ~22 registers out of the traversal loop and so raises occupancy; the loop is
+// latency-bound.  Kernels using HddaAn launch 1-D blocks of at most kGeomBlock threads.
+constexpr int kGeomBlock = 128;
+struct HddaGeomSmem {
+    double e[3][kGeomBlock], dv[3][kGeomBlock], iv[3][kGeomBlock];
+    double te[kGeomBlock], tx[kGeomBlock];
+    int m[3][kGeomBlock];
+};
+__device__ __forceinline__ HddaGeomSmem& hdda_geom() {
+    __shared__ HddaGeomSmem g;
+    return g;
+}
+#endif
+
 struct HddaAn {
     static constexpr bool kHdda = true;
+#if SOGK_HDDA_SMEM
+    __device__ __forceinline__ double& E(int a) { return hdda_geom().e[a][threadIdx.x]; }
+    __device__ __forceinline__ double& DV(int a) { return hdda_geom().dv[a][threadIdx.x]; }
+    __device__ __forceinline__ double& IV(int a) { return hdda_geom().iv[a][threadIdx.x]; }
+    __device__ __forceinline__ int& M(int a) { return hdda_geom().m[a][threadIdx.x]; }
+    __device__ __forceinline__ double& TE() { return hdda_geom().te[threadIdx.x]; }
+    __device__ __forceinline__ double& TX() { return hdda_geom().tx[threadIdx.x]; }
+    __device__ __forceinline__ double TE() const { return hdda_geom().te[threadIdx.x]; }
+    __device__ __forceinline__ double TX() const { return hdda_geom().tx[threadIdx.x]; }
+#else
     double e[3], dv[3], iv[3]; // mirrored entry, |dir|, 1/|dir|
     int m[3];                  // -1 on mirrored axes, else 0
     double t_enter, t_exit;
+    __device__ __forceinline__ double& E(int a) { return e[a]; }
+    __device__ __forceinline__ double& DV(int a) { return dv[a]; }
+    __device__ __forceinline__ double& IV(int a) { return iv[a]; }
+    __device__ __forceinline__ int& M(int a) { return m[a]; }
+    __device__ __forceinline__ double& TE() { return t_enter; }
+    __device__ __forceinline__ double& TX() { return t_exit; }
+    __device__ __forceinline__ double TE() const { return t_enter; }
+    __device__ __forceinline__ double TX() const { return t_exit; }
+#endif
     bool valid;
     int ijk[3];
     double t_cur;
@@ -402,8 +440,8 @@ struct HddaAn {
         Geom geom;
         geom.init(r, g);
         valid = geom.valid;
-        t_enter = geom.t_enter;
-        t_exit = geom.t_exit;
+        TE() = geom.t_enter;
+        TX() = geom.t_exit;
         done = !valid;
         if (done) return;
         geom.entry_cell(g.res, ijk);
@@ -411,20 +449,20 @@ struct HddaAn {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             if (geom.step[a] > 0) {
-                e[a] = geom.entry[a];
-                dv[a] = geom.dir[a];
-                iv[a] = geom.inv[a];
-                m[a] = 0;
+                E(a) = geom.entry[a];
+                DV(a) = geom.dir[a];
+                IV(a) = geom.inv[a];
+                M(a) = 0;
             } else if (geom.step[a] < 0) {
-                e[a] = -geom.entry[a];
-                dv[a] = -geom.dir[a];
-                iv[a] = -geom.inv[a];
-                m[a] = -1;
+                E(a) = -geom.entry[a];
+                DV(a) = -geom.dir[a];
+                IV(a) = -geom.inv[a];
+                M(a) = -1;
             } else {
-                e[a] = (double)ijk[a] + 0.5;
-                dv[a] = 0.0;
-                iv[a] = __longlong_as_double(0x7ff0000000000000ll); // +inf
-                m[a] = 0;
+                E(a) = (double)ijk[a] + 0.5;
+                DV(a) = 0.0;
+                IV(a) = __longlong_as_double(0x7ff0000000000000ll); // +inf
+                M(a) = 0;
             }
         }
     }
@@ -437,34 +475,36 @@ struct HddaAn {
         ++lookups;
         // exit plane of the node on each axis (:218-228), mirrored: lo + ext walking up,
         // -lo walking down; the cell just past it (`stepped`, :236-237) is plane' ^ m
+        const double te = TE();
         double tc[3];
         int pl[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const int lo = ijk[a] & -q.ext;
             ev.ijk[a] = lo;
-            pl[a] = (lo ^ m[a]) + (m[a] ? 1 : q.ext);
-            tc[a] = t_enter + ((double)pl[a] - e[a]) * iv[a];
+            pl[a] = (lo ^ M(a)) + (M(a) ? 1 : q.ext);
+            tc[a] = te + ((double)pl[a] - E(a)) * IV(a);
         }
         double t1;
         const int axis = argmin3(tc[0], tc[1], tc[2], t1);
         ev.level = q.level;
         ev.occ = q.occ;
-        if (t1 >= t_exit) {
+        const double tx = TX();
+        if (t1 >= tx) {
             ++steps;
             done = true;
             ev.t0 = t_cur;
-            ev.t1 = t_exit;
+            ev.t1 = tx;
             return 1;
         }
         const bool degen = t1 <= t_cur; // degenerate corner crossing (:238-241)
         // cell_after_crossing (:91-104) at t_cur (degenerate) or t1, all axes
         // evaluated and the stepped one overridden
-        const double dt = (degen ? t_cur : t1) - t_enter;
+        const double dt = (degen ? t_cur : t1) - te;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const int c = __double2int_rd(e[a] + dt * dv[a]) ^ m[a];
-            ijk[a] = (a == axis) ? (pl[a] ^ m[a]) : c;
+            const int c = __double2int_rd(E(a) + dt * DV(a)) ^ M(a);
+            ijk[a] = (a == axis) ? (pl[a] ^ M(a)) : c;
         }
         if (degen) {
             // the reference spins forever at exact edge crossings
@@ -500,8 +540,8 @@ struct HddaAn {
     }
 
     __device__ __forceinline__ bool is_valid() const { return valid; }
-    __device__ __forceinline__ double enter_t() const { return t_enter; }
-    __device__ __forceinline__ double exit_t() const { return t_exit; }
+    __device__ __forceinline__ double enter_t() const { return TE(); }
+    __device__ __forceinline__ double exit_t() const { return TX(); }
 };
 
 // CascadeTraversal<GridT>, sampling.hpp:305-415, over SOGK_MAX_LEVELS levels

@@ -213,11 +213,24 @@ __device__ __forceinline__ void count_invalid(long long r, int64_t* packed, uint
 // ---------------------------------------------------------------------------
 // pass 1: per-ray counts, status, counters, slab samples, resume state
 // ---------------------------------------------------------------------------
+// Pass-1 slab staging: a lane puts its samples in a 4-slot shared-memory group (SoA,
+// conflict-free) and writes each group of 4 slab entries as one 256-bit (t) and one 128-bit
+// (cell) store; slab rows are 32-byte aligned (C is a multiple of 4).
+__device__ __forceinline__ void stage_flush(const SlabDev& S, int64_t idx, const double* st,
+                                            const uint32_t* sc) {
+    static_cast<double4*>(__builtin_assume_aligned(S.t + idx, 32))[0] =
+        make_double4(st[0], st[kBlock], st[2 * kBlock], st[3 * kBlock]);
+    static_cast<uint4*>(__builtin_assume_aligned(S.cell + idx, 16))[0] =
+        make_uint4(sc[0], sc[kBlock], sc[2 * kBlock], sc[3 * kBlock]);
+}
+
 template <int AN, bool CASC, bool BR, int SCH, class Src>
 __global__ void __launch_bounds__(kBlock, SOGK_COUNT_MINB)
     count_kernel(const SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
                  int32_t* __restrict__ counters, const SlabDev S) {
+    __shared__ double stage_t[4 * kBlock];
+    __shared__ uint32_t stage_c[4 * kBlock];
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     Stats5 acc;
     if (r < n) {
@@ -232,6 +245,9 @@ __global__ void __launch_bounds__(kBlock, SOGK_COUNT_MINB)
             int filled = 0;     // samples in the slab
             bool ovf = false;   // slab full: the rest of the ray comes from its resume state
             bool stored = false;
+            bool tail_flushed = false; // the group holding the slab's last sample is written
+            double* const st_t = stage_t + threadIdx.x;
+            uint32_t* const st_c = stage_c + threadIdx.x;
             for (;;) { // one flat loop: one analyzer step per iteration
                 Event ev;
                 double t_last0;
@@ -240,21 +256,28 @@ __global__ void __launch_bounds__(kBlock, SOGK_COUNT_MINB)
                 if (st == 1) continue;
                 int k = 0; // points of this event
                 if (!ovf) { // the reference loop itself: while (t <= t1) { push(t); t += step(t); }
-                    const uint32_t cell = pack_cell(ev.ijk);
+                    // single grids: the 2-bit Level rides in the cell word's spare top bits
+                    // (cells pack 3 x 10 bits); cascades also need grid_level, in S.lvl
+                    const uint32_t cw = CASC ? pack_cell(ev.ijk)
+                                             : pack_cell(ev.ijk) | ((uint32_t)ev.level << 30);
                     const uint8_t lvl = (uint8_t)(ev.level | (ev.grid_level << 2));
                     double t = gen.t_last;
-                    const int64_t base = row + filled;
                     const int room = (int)S.C - filled;
                     while (t <= ev.t1 && k < room) {
-                        S.t[base + k] = t;
-                        S.cell[base + k] = cell;
-                        S.lvl[base + k] = lvl;
+                        const int p = filled + k;
+                        st_t[(p & 3) * kBlock] = t;
+                        st_c[(p & 3) * kBlock] = cw;
+                        if (CASC) S.lvl[row + p] = lvl;
+                        if ((p & 3) == 3) stage_flush(S, row + p - 3, st_t, st_c);
                         t = t + ladder_step<SCH>(t, s.dt0, s.growth);
                         ++k;
                     }
                     gen.t_last = t;
                     if (t <= ev.t1) { // slab full inside this event: it restarts in tail_kernel
                         ovf = true;
+                        // this event's samples may have recycled the staging slots of the
+                        // group holding position filled - 1; that group was written whole first
+                        tail_flushed = filled + k >= (filled & ~3) + 4;
                         Run run;
                         run.ijk[0] = ev.ijk[0];
                         run.ijk[1] = ev.ijk[1];
@@ -272,6 +295,8 @@ __global__ void __launch_bounds__(kBlock, SOGK_COUNT_MINB)
                 if (BR) gen.kernel_lookups += k;
                 c += k;
             }
+            // the partial last group (a slab row is private to its ray: written whole)
+            if ((filled & 3) && !tail_flushed) stage_flush(S, row + (filled & ~3), st_t, st_c);
             count_finish(gen, r, c, packed, status, counters, acc);
             if (stored && c > 0 && !gen.undefined()) {
                 S.ovf_list[atomicAdd(S.ovf_ctr, 1u)] = (uint32_t)r;
@@ -492,7 +517,7 @@ __global__ void __launch_bounds__(kWriteBlock)
 // over the block's offsets in shared memory.  Samples past a ray's slab are tail_kernel's.
 constexpr int kGather = 256;
 
-template <int SCH>
+template <int SCH, bool CASC>
 __global__ void __launch_bounds__(kGather)
     gather_kernel(const SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
                   const SlabDev S, int64_t ray_index_base, const Out o) {
@@ -529,8 +554,9 @@ __global__ void __launch_bounds__(kGather)
         __stcs(o.t_starts + g, t);
         if (o.t_ends) __stcs(o.t_ends + g, t + ladder_step<SCH>(t, s.dt0, s.growth));
         if (o.ray_indices) __stcs(o.ray_indices + g, (int32_t)(ray_index_base + r0 + j));
-        if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, __ldcs(reinterpret_cast<const unsigned int*>(S.cell) + i));
-        if (o.levels) o.levels[g] = S.lvl[i];
+        const uint32_t cw = __ldcs(reinterpret_cast<const unsigned int*>(S.cell) + i);
+        if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, CASC ? cw : cw & 0x3fffffffu);
+        if (o.levels) o.levels[g] = CASC ? S.lvl[i] : (uint8_t)(cw >> 30);
     }
 }
 
@@ -625,7 +651,7 @@ struct Launch {
             return cudaGetLastError();
         }
         const unsigned gb = (unsigned)((n + kGather - 1) / kGather);
-        gather_kernel<SCH><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
+        gather_kernel<SCH, CASC><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
         const unsigned tg = tail_grid(n);
         if (vec)
             tail_kernel<AN, CASC, BR, SCH, true, Src><<<tg, kWriteBlock, 0, st>>>(s, src, packed, *S, base, o);
