@@ -541,22 +541,48 @@ __global__ void __launch_bounds__(kGather)
     s_fill[tid] = fill;
     __syncthreads();
     const int m = (int)(O1 - O0);
-    for (int e = tid; e < m; e += kGather) {
-        int j = 0; // largest j with s_off[j] <= e: branch-free binary search over 256 entries
+    // kUnroll independent samples per thread and iteration (stride kGather: stores stay
+    // coalesced), so each thread keeps several slab loads in flight
+    constexpr int kUnroll = 4;
+    for (int e0 = tid; e0 < m; e0 += kUnroll * kGather) {
+        int j[kUnroll], k[kUnroll];
+        bool ok[kUnroll];
 #pragma unroll
-        for (int step = kGather / 2; step > 0; step >>= 1)
-            j += (s_off[j + step] <= e) ? step : 0;
-        const int k = e - s_off[j];
-        if (k >= s_fill[j]) continue;
-        const int64_t i = (r0 + j) * S.C + k;
-        const long long g = O0 + e;
-        const double t = __ldcs(S.t + i);
-        __stcs(o.t_starts + g, t);
-        if (o.t_ends) __stcs(o.t_ends + g, t + ladder_step<SCH>(t, s.dt0, s.growth));
-        if (o.ray_indices) __stcs(o.ray_indices + g, (int32_t)(ray_index_base + r0 + j));
-        const uint32_t cw = __ldcs(reinterpret_cast<const unsigned int*>(S.cell) + i);
-        if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, CASC ? cw : cw & 0x3fffffffu);
-        if (o.levels) o.levels[g] = CASC ? S.lvl[i] : (uint8_t)(cw >> 30);
+        for (int u = 0; u < kUnroll; ++u) {
+            const int e = e0 + u * kGather;
+            int jj = 0; // largest jj with s_off[jj] <= e: branch-free binary search
+#pragma unroll
+            for (int step = kGather / 2; step > 0; step >>= 1)
+                jj += (s_off[jj + step] <= e) ? step : 0;
+            j[u] = jj;
+            k[u] = e - s_off[jj];
+            ok[u] = e < m && k[u] < s_fill[jj];
+        }
+        double t[kUnroll];
+        uint32_t cw[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            t[u] = 0.0;
+            cw[u] = 0;
+            if (ok[u]) {
+                const int64_t i = (r0 + j[u]) * S.C + k[u];
+                t[u] = __ldcs(S.t + i);
+                cw[u] = __ldcs(reinterpret_cast<const unsigned int*>(S.cell) + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (!ok[u]) continue;
+            const long long g = O0 + e0 + u * kGather;
+            __stcs(o.t_starts + g, t[u]);
+            if (o.t_ends) __stcs(o.t_ends + g, t[u] + ladder_step<SCH>(t[u], s.dt0, s.growth));
+            if (o.ray_indices) __stcs(o.ray_indices + g, (int32_t)(ray_index_base + r0 + j[u]));
+            if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, CASC ? cw[u] : cw[u] & 0x3fffffffu);
+            if (o.levels) {
+                const int64_t i = (r0 + j[u]) * S.C + k[u];
+                o.levels[g] = CASC ? S.lvl[i] : (uint8_t)(cw[u] >> 30);
+            }
+        }
     }
 }
 
