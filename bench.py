@@ -406,24 +406,33 @@ def run_gpu(args):
     samples_s = h["samples"] / sec
     peak, peak_src = load_peaks()
     # roofline: dominant kernel (larger share of the step) with its algorithmic bytes
+    # (SURVEY §8(d)): pass 1 reads the rays (64 B) and writes packed_info (16 B) per ray;
+    # pass 2 reads packed_info (16 B/ray) and writes the samples (24 B each).  The slabs
+    # pass 1 hands to pass 2 (12 B/sample each way) are not algorithmic; ncu's DRAM bytes
+    # (`traffic`, profiles/traffic_<cfg>.json) show them.
     launches = args.steps * n_obj
     nr_loc = nr * n_obj * args.steps
-    write_bytes = nr_loc * 16 + h["local_samples"] * 24  # packed_info read + samples written
+    write_bytes = nr_loc * 16 + h["local_samples"] * 24
     count_bytes = nr_loc * (64 + 16)
-    if h["write_ms"] >= h["count_ms"]:
-        dom, dom_ms, dom_bytes = "expand_kernel + tail_kernel (pass 2)", h["write_ms"], write_bytes
-    else:
-        dom, dom_ms, dom_bytes = "count_kernel (pass 1 + fused scan)", h["count_ms"], count_bytes
-    achieved = dom_bytes / launches / (dom_ms / launches / 1e3) / 1e9
+    pass2 = {"kernel": "gather_kernel + tail_kernel (pass 2)", "ms": h["write_ms"], "bytes": write_bytes}
+    pass1 = {"kernel": "count_kernel + scan_kernel (pass 1)", "ms": h["count_ms"], "bytes": count_bytes}
+    dom, other = (pass2, pass1) if h["write_ms"] >= h["count_ms"] else (pass1, pass2)
+
+    def gbs(k):
+        return k["bytes"] / launches / (k["ms"] / launches / 1e3) / 1e9
+
+    achieved = gbs(dom)
     step_bytes = nr_loc * (64 + 16) + h["local_samples"] * 24 + sum(vdb_bytes) * args.steps
     step_gbs = step_bytes / (h["ms"] / 1e3) / 1e9
-    traffic = None
+    traffic = {}
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tf))
         except Exception:
-            traffic = None
+            traffic = {}
+    dom_key = "pass1" if dom is pass1 else "pass2"
+    other_key = "pass2" if dom is pass1 else "pass1"
 
     line = {
         "metric": "rays/sec and samples/sec per B200 (and 8-GPU box), HDDA-VDB vs dense-DDA, % HBM roofline",
@@ -450,9 +459,15 @@ def run_gpu(args):
                          "count_ms_per_step": v["count_ms"] / args.steps,
                          "write_ms_per_step": v["write_ms"] / args.steps} for k, v in agg.items()},
         "hdda_vs_dda_branch": (agg["dda_branch"]["ms"] / agg["hdda_skip"]["ms"]) if {"dda_branch", "hdda_skip"} <= agg.keys() else None,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": dom_bytes / launches},
+        "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic.get(dom_key, {}).get("dram_bytes_per_launch"),
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": dom["bytes"] / launches,
+                     "note": "pass 1 is bound by traversal issue/latency and L1/L2 store transactions, "
+                             "not HBM (DESIGN.md §4); traffic = ncu dram read+write of one launch "
+                             "(object 0), " + traffic.get("source", "no capture committed"),
+                     "other_pass": {"kernel": other["kernel"], "achieved": gbs(other), "frac": gbs(other) / peak,
+                                    "algorithmic_bytes_per_launch": other["bytes"] / launches,
+                                    "traffic": traffic.get(other_key, {}).get("dram_bytes_per_launch")}},
         "step_roofline": {"bytes_per_step": step_bytes / args.steps, "achieved_gbs": step_gbs,
                           "frac": step_gbs / peak,
                           "basis": "N_rays*(64+16) + N_samples*24 + VDB bytes (SURVEY §8d)"},
@@ -587,7 +602,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default per config, a timed region of >= ~150 ms: cfg1/cfg3 200, cfg2 50, cfg4 10)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
@@ -596,6 +612,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = {"cfg1": 200, "cfg2": 50, "cfg3": 200, "cfg4": 10}[args.config]
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
