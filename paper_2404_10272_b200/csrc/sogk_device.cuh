@@ -544,25 +544,48 @@ struct HddaAn {
     __device__ __forceinline__ double exit_t() const { return TX(); }
 };
 
-// CascadeTraversal<GridT>, sampling.hpp:305-415, over SOGK_MAX_LEVELS levels
+// CascadeTraversal<GridT>, sampling.hpp:305-415, over SOGK_MAX_LEVELS levels.
+// Every loop over levels and cuts has a fixed trip count (unrolled, guarded by n_levels)
+// and the cut list is sorted by a sorting network, so nothing here is dynamically indexed
+// in registers: the sorted cut list and the ray live in per-thread shared-memory columns,
+// the segment levels in one packed register.  (Dynamic indexing sent the whole analyzer,
+// sub-analyzer included, to local memory.)
+constexpr int kCascadeCuts = 2 * SOGK_MAX_LEVELS; // te, tx + 2 per inner level
+
+struct CascadeSmem {
+    double cut[kCascadeCuts][kGeomBlock];
+    double od[6][kGeomBlock]; // ray origin, direction
+};
+__device__ __forceinline__ CascadeSmem& cascade_smem() {
+    __shared__ CascadeSmem c;
+    return c;
+}
+
+__device__ __forceinline__ void cmp_swap(double& a, double& b) {
+    const double lo = (b < a) ? b : a, hi = (b < a) ? a : b;
+    a = lo;
+    b = hi;
+}
+
 template <class Sub>
 struct CascadeAn {
-    static constexpr int kMaxSeg = 2 * SOGK_MAX_LEVELS;
-    Ray ray;
-    double cut[kMaxSeg + 2];
-    signed char seg_level[kMaxSeg + 1];
+    unsigned seg_lv;       // 3 bits per segment: grid level + 1 (0: outside every level)
     int n_seg, seg;
     bool has_sub;
+    int cur_gl;            // grid level of the open segment
+    const GridDev* cur_g;  // &s.lv[cur_gl] (a __grid_constant__ parameter)
     Sub sub;
     int fin_lookups, fin_steps;
     bool valid;
     bool undefined;
     double t_enter, t_exit;
 
+    __device__ __forceinline__ double& CUT(int i) { return cascade_smem().cut[i][threadIdx.x]; }
+
     __device__ __forceinline__ void init(const Ray& r, const SamplerDev& s) { // :312-355
-        ray = r;
         n_seg = 0;
         seg = 0;
+        seg_lv = 0;
         has_sub = false;
         fin_lookups = fin_steps = 0;
         valid = false;
@@ -571,55 +594,84 @@ struct CascadeAn {
         const int n = s.n_levels;
         double rf[SOGK_MAX_LEVELS], rs[SOGK_MAX_LEVELS];
         bool hit[SOGK_MAX_LEVELS];
-        for (int b = 0; b < n; ++b) hit[b] = clip_to_box(r, s.lv[b].clo, s.lv[b].chi, rf[b], rs[b]);
-        if (!hit[n - 1]) return;
-        const double te = rf[n - 1], tx = rs[n - 1];
-        double cuts[kMaxSeg + 2];
-        int nc = 0;
-        cuts[nc++] = te;
-        cuts[nc++] = tx;
-        for (int b = 0; b + 1 < n; ++b) {
-            if (!hit[b]) continue;
-            if (rf[b] > te && rf[b] < tx) cuts[nc++] = rf[b];
-            if (rs[b] > te && rs[b] < tx) cuts[nc++] = rs[b];
-        }
-        for (int i = 1; i < nc; ++i) { // std::sort
-            const double v = cuts[i];
-            int j = i - 1;
-            while (j >= 0 && cuts[j] > v) {
-                cuts[j + 1] = cuts[j];
-                --j;
+        double te = 0.0, tx = 0.0;
+        bool hit_last = false;
+#pragma unroll
+        for (int b = 0; b < SOGK_MAX_LEVELS; ++b) {
+            rf[b] = rs[b] = 0.0;
+            hit[b] = b < n && clip_to_box(r, s.lv[b].clo, s.lv[b].chi, rf[b], rs[b]);
+            if (b == n - 1) {
+                hit_last = hit[b];
+                te = rf[b];
+                tx = rs[b];
             }
-            cuts[j + 1] = v;
         }
-        int m = 0; // std::unique
-        for (int i = 0; i < nc; ++i)
-            if (m == 0 || !(cuts[m - 1] == cuts[i])) cuts[m++] = cuts[i];
-        // after unique the cuts are strictly increasing, so every pair is a segment
-        for (int i = 0; i + 1 < m; ++i) {
-            if (!(cuts[i] < cuts[i + 1])) continue;
-            const double mid = 0.5 * (cuts[i] + cuts[i + 1]);
-            int level = -1;
-            for (int b = 0; b < n; ++b)
-                if (hit[b] && mid >= rf[b] && mid < rs[b]) {
-                    level = b;
-                    break;
-                }
-            cut[n_seg] = cuts[i];
-            cut[n_seg + 1] = cuts[i + 1];
-            seg_level[n_seg] = (signed char)level;
-            ++n_seg;
+        if (!hit_last) return;
+        // cuts: te, tx and every inner boundary strictly inside (te, tx); +inf = absent
+        const double inf = __longlong_as_double(0x7ff0000000000000ll);
+        double c[kCascadeCuts];
+        c[0] = te;
+        c[1] = tx;
+#pragma unroll
+        for (int b = 0; b + 1 < SOGK_MAX_LEVELS; ++b) {
+            const bool use = b + 1 < n && hit[b];
+            c[2 + 2 * b] = (use && rf[b] > te && rf[b] < tx) ? rf[b] : inf;
+            c[3 + 2 * b] = (use && rs[b] > te && rs[b] < tx) ? rs[b] : inf;
+        }
+        // std::sort: odd-even transposition network (fixed size, all indices constant)
+#pragma unroll
+        for (int pass = 0; pass < kCascadeCuts; ++pass) {
+#pragma unroll
+            for (int i = pass & 1; i + 1 < kCascadeCuts; i += 2) cmp_swap(c[i], c[i + 1]);
+        }
+        // std::unique, then one segment per consecutive pair; level = the finest level whose
+        // voxel-centre box holds the segment midpoint (:340-351)
+        int m = 0;
+        double prev = 0.0;
+#pragma unroll
+        for (int i = 0; i < kCascadeCuts; ++i) {
+            const double v = c[i];
+            if (v == inf) continue;
+            if (m > 0 && v == prev) continue;
+            if (m > 0) {
+                const double mid = 0.5 * (prev + v);
+                int level = -1;
+#pragma unroll
+                for (int b = SOGK_MAX_LEVELS - 1; b >= 0; --b)
+                    if (b < n && hit[b] && mid >= rf[b] && mid < rs[b]) level = b;
+                seg_lv |= (unsigned)(level + 1) << (3 * (m - 1));
+            }
+            CUT(m) = v;
+            prev = v;
+            ++m;
+        }
+        n_seg = m - 1;
+        CascadeSmem& cs = cascade_smem();
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            cs.od[a][threadIdx.x] = r.o[a];
+            cs.od[3 + a][threadIdx.x] = r.d[a];
         }
         valid = n_seg > 0;
         t_enter = te;
         t_exit = tx;
     }
 
+    __device__ __forceinline__ int seg_level(int i) const { return (int)((seg_lv >> (3 * i)) & 7u) - 1; }
+
     __device__ __forceinline__ void open_sub(const SamplerDev& s) {
-        Ray sr = ray; // Ray(origin, dir, seg.t0, seg.t1) (:389-390)
-        sr.tmin = cut[seg];
-        sr.tmax = cut[seg + 1];
-        sub.init(sr, s.lv[seg_level[seg]], s.spin_cap);
+        Ray sr; // Ray(origin, dir, seg.t0, seg.t1) (:389-390)
+        const CascadeSmem& cs = cascade_smem();
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            sr.o[a] = cs.od[a][threadIdx.x];
+            sr.d[a] = cs.od[3 + a][threadIdx.x];
+        }
+        sr.tmin = CUT(seg);
+        sr.tmax = CUT(seg + 1);
+        cur_gl = seg_level(seg);
+        cur_g = &s.lv[cur_gl];
+        sub.init(sr, *cur_g, s.spin_cap);
         has_sub = true;
     }
 
@@ -627,10 +679,9 @@ struct CascadeAn {
     // -1 = internal transition (sub-analyzer step, segment change) — call again.
     __device__ __forceinline__ int next(const SamplerDev& s, Event& ev) {
         if (has_sub) {
-            const int gl = seg_level[seg];
-            const int r = sub.next(s.lv[gl], ev);
+            const int r = sub.next(*cur_g, ev);
             if (r != 0) {
-                ev.grid_level = gl;
+                ev.grid_level = cur_gl;
                 return r;
             }
             if (sub.undefined) {
@@ -644,12 +695,12 @@ struct CascadeAn {
             return -1;
         }
         if (seg >= n_seg) return 0;
-        const int gl = seg_level[seg];
+        const int gl = seg_level(seg);
         if (gl < 0) { // outside every level: one empty event
             ev.ijk[0] = ev.ijk[1] = ev.ijk[2] = 0;
             ev.level = LV_ROOT_TILE;
-            ev.t0 = cut[seg];
-            ev.t1 = cut[seg + 1];
+            ev.t0 = CUT(seg);
+            ev.t1 = CUT(seg + 1);
             ev.occ = false;
             ev.grid_level = -1;
             ++seg;
@@ -666,7 +717,7 @@ struct CascadeAn {
                                             double in_t) {
         seg = tag;
         open_sub(s);
-        sub.restore(s.lv[seg_level[seg]], in_ijk, in_t);
+        sub.restore(*cur_g, in_ijk, in_t);
     }
 
     __device__ __forceinline__ int lookup_count() const {

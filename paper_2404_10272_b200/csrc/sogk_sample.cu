@@ -23,6 +23,9 @@ namespace sogk {
 
 constexpr int kBlock = 128;
 constexpr int kWriteBlock = 128;
+#ifndef SOGK_CASC_MINB
+#define SOGK_CASC_MINB 1 // the same for the cascade variants
+#endif
 #ifndef SOGK_COUNT_MINB
 #define SOGK_COUNT_MINB 1 // pass-1 min resident blocks per SM (register cap), A/B-tunable
 #endif
@@ -225,8 +228,8 @@ __device__ __forceinline__ void stage_flush(const SlabDev& S, int64_t idx, const
 }
 
 template <int AN, bool CASC, bool BR, int SCH, class Src>
-__global__ void __launch_bounds__(kBlock, SOGK_COUNT_MINB)
-    count_kernel(const SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
+__global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MINB)
+    count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
                  int32_t* __restrict__ counters, const SlabDev S) {
     __shared__ double stage_t[4 * kBlock];
@@ -488,7 +491,7 @@ struct LaneWriter {
 // cold path: no pass-1 slabs for these rays, traverse from the start
 template <int AN, bool CASC, bool BR, int SCH, bool VEC, class Src>
 __global__ void __launch_bounds__(kWriteBlock)
-    write_kernel(const SamplerDev s, const Src src, int64_t n, const int64_t* __restrict__ packed,
+    write_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, const int64_t* __restrict__ packed,
                  int64_t ray_index_base, const Out o) {
     const int64_t r = (int64_t)blockIdx.x * kWriteBlock + threadIdx.x;
     if (r >= n) return;
@@ -519,7 +522,7 @@ constexpr int kGather = 256;
 
 template <int SCH, bool CASC>
 __global__ void __launch_bounds__(kGather)
-    gather_kernel(const SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
+    gather_kernel(const __grid_constant__ SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
                   const SlabDev S, int64_t ray_index_base, const Out o) {
     __shared__ long long s_base[2];
     __shared__ int s_off[kGather]; // ray offsets relative to the block's first sample
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(kGather)
 // did not fit and write the rest of the ray directly
 template <int AN, bool CASC, bool BR, int SCH, bool VEC, class Src>
 __global__ void __launch_bounds__(kWriteBlock)
-    tail_kernel(const SamplerDev s, const Src src, const int64_t* __restrict__ packed,
+    tail_kernel(const __grid_constant__ SamplerDev s, const Src src, const int64_t* __restrict__ packed,
                 const SlabDev S, int64_t ray_index_base, const Out o) {
     const unsigned cnt = *S.ovf_ctr;
     for (unsigned i = blockIdx.x * kWriteBlock + threadIdx.x; i < cnt; i += gridDim.x * kWriteBlock) {
