@@ -212,6 +212,40 @@ int sogk_camera_rays(const sogk_camera* cam, int64_t first_pixel, int64_t n, dou
 int sogk_camera_rays_host(const sogk_camera* cam, int64_t first_pixel, int64_t n,
                           double* h_rays);
 
+/* ---- compositing consumer (render.hpp) -----------------------------------
+ * The emission-absorption renderer the reference composites sample buffers with. */
+enum { SOGK_SPHERE = 0, SOGK_BOX = 1 };
+/* sog::Primitive (render.hpp:19-56) */
+typedef struct {
+    int32_t shape;          /* SOGK_SPHERE / SOGK_BOX */
+    double center[3];       /* sphere */
+    double radius;          /* sphere */
+    double lo[3], hi[3];    /* box, half-open */
+    double density;         /* sigma >= 0 */
+    double color[3];        /* in [0, 1] */
+} sogk_primitive;
+typedef struct sogk_scene sogk_scene; /* sog::AnalyticScene (render.hpp:58-92) in HBM */
+
+/* AnalyticScene::validate (render.hpp:62-70) + upload; n may be 0 (background only) */
+int sogk_scene_create(const sogk_primitive* h_prims, int32_t n, const double background[3],
+                      sogk_scene** out);
+int sogk_scene_destroy(sogk_scene* scene);
+
+/* composite_detailed (render.hpp:97-118) of every ray of a packed batch (the output of
+ * sogk_sample_count/write on the same rays): d_result[n][5] = color r, g, b, weight_sum,
+ * transmittance; d_rgb8[n][3] (optional) = Image::set_pixel bytes (render.hpp:133-139).
+ * dt of sample i is t[i+1] - t[i], of the last the schedule's step (render.hpp:106). */
+int sogk_composite(const sogk_sampler* s, const sogk_scene* scene, const double* d_rays, int64_t n,
+                   const int64_t* d_packed_info, const double* d_t_starts, double* d_result,
+                   uint8_t* d_rgb8, void* stream);
+/* render_frame's per-pixel work (bench.hpp:424-461) fused into one kernel: each pixel's ray
+ * is generated, sampled and composited in registers, no sample array is written.
+ * d_stats: SOGK_STAT_TOTAL_SAMPLES, _ANALYZER_LOOKUPS, _ANALYZER_STEPS, _KERNEL_LOOKUPS,
+ * _UNDEFINED_RAYS of the pixels (FrameResult lookups / steps / samples). */
+int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_camera* cam,
+                       int64_t first_pixel, int64_t n, double* d_result, uint8_t* d_rgb8,
+                       int64_t* d_stats, void* stream);
+
 /* ---- host input generators (deterministic; no GPU needed) ---------------
  * Restatements of the reference generators so that identical inputs can be
  * produced where the reference is absent (tests pin them to the reference). */
@@ -223,6 +257,11 @@ int sogk_scene_generate(int kind, const sogk_transform* t, uint64_t seed, double
 int sogk_scene_cascade(int kind, const sogk_transform* base, uint64_t seed, double fraction,
                        int32_t count, double threshold, int32_t levels, uint8_t* h_bits,
                        sogk_transform* out_transforms);
+/* generate_scene's AnalyticScene (scene_gen.hpp:94-176, background :112): the primitives the
+ * occupancy is rasterized from.  h_prims == NULL: size query (*n_prims only). */
+int sogk_scene_analytic(int kind, const sogk_transform* t, uint64_t seed, int32_t count,
+                        sogk_primitive* h_prims, int32_t cap, int32_t* n_prims,
+                        double background[3]);
 /* make_probe_rays (bench.hpp:628-649) */
 int sogk_probe_rays(const sogk_transform* t, int64_t count, uint64_t seed, double* h_rays);
 /* testsupport::random_ray x count from one mt19937_64(seed) (tests/support/test_support.hpp:66-82) */

@@ -417,4 +417,86 @@ double ref_time_sampler(void* h, const double* rays, int64_t n, const uint8_t* s
     return secs[secs.size() / 2];
 }
 
+// generate_scene's AnalyticScene (scene_gen.hpp:94-176): 16 doubles per primitive =
+// shape, center[3], radius, lo[3], hi[3], density, color[3], 0; returns the count
+int ref_scene_primitives(int kind, const int32_t res[3], const double wmin[3], double voxel,
+                         uint64_t seed, double fraction, int count, double* out, int cap,
+                         double* background) {
+    SceneParams p;
+    p.seed = seed;
+    p.fraction = fraction;
+    p.primitive_count = count;
+    const GeneratedScene gen = generate_scene(SceneKind(kind), make_transform(res, wmin, voxel), p);
+    const auto& prims = gen.scene.primitives;
+    for (int a = 0; a < 3; ++a) background[a] = gen.scene.background[a];
+    for (int i = 0; i < int(prims.size()) && i < cap; ++i) {
+        const Primitive& q = prims[i];
+        double* o = out + 16 * i;
+        o[0] = q.shape == Primitive::Shape::sphere ? 0.0 : 1.0;
+        for (int a = 0; a < 3; ++a) {
+            o[1 + a] = q.center[a];
+            o[5 + a] = q.lo[a];
+            o[8 + a] = q.hi[a];
+            o[12 + a] = q.color[a];
+        }
+        o[4] = q.radius;
+        o[11] = q.density;
+        o[15] = 0.0;
+    }
+    return int(prims.size());
+}
+
+// render_frame (bench.hpp:424-461) of one bench variant on build_assets(cfg)
+// (bench.hpp:306-376): rgb = width*height*3 bytes; stats = lookups, steps, samples
+void ref_render_frame(int kind, uint64_t seed, double fraction, int resolution, int cascades,
+                      int sched_kind, int width, int height, int grid, int analyzer, int kernel,
+                      int threads, uint8_t* rgb, int64_t* stats) {
+    BenchConfig cfg;
+    cfg.kind = SceneKind(kind);
+    cfg.params.seed = seed;
+    if (fraction > 0.0) cfg.params.fraction = fraction;
+    cfg.resolution = resolution;
+    cfg.cascades = cascades;
+    cfg.schedule_kind = sched_kind == 0 ? StepSchedule::Kind::constant : StepSchedule::Kind::linear;
+    cfg.width = width;
+    cfg.height = height;
+    const BenchAssets assets = build_assets(cfg);
+    const VariantId v{grid == 0 ? GridKind::dense : GridKind::sparse,
+                      analyzer == 0 ? AnalyzerKind::dda : AnalyzerKind::hdda,
+                      kernel == 0 ? KernelKind::branch : KernelKind::skip};
+    const FrameResult f = render_frame(assets, make_sampler(assets, v), threads);
+    std::memcpy(rgb, f.image.data().data(), f.image.data().size());
+    stats[0] = f.lookups;
+    stats[1] = f.steps;
+    stats[2] = f.samples;
+}
+
+// composite_detailed (render.hpp:97-118) through the reference: prims as 16 doubles each
+// (ref_scene_primitives layout); out = color rgb, weight_sum, transmittance
+void ref_composite(const double* ray, const double* samples, int64_t n, const double* prims,
+                   int n_prims, const double* background, int sched_kind, double dt0,
+                   double growth, double* out) {
+    AnalyticScene scene;
+    scene.background = {background[0], background[1], background[2]};
+    for (int i = 0; i < n_prims; ++i) {
+        const double* q = prims + 16 * i;
+        const Vec3 color{q[12], q[13], q[14]};
+        if (q[0] == 0.0)
+            scene.primitives.push_back(Primitive::sphere({q[1], q[2], q[3]}, q[4], q[11], color));
+        else
+            scene.primitives.push_back(
+                Primitive::box({q[5], q[6], q[7]}, {q[8], q[9], q[10]}, q[11], color));
+    }
+    const Ray r({ray[0], ray[1], ray[2]}, {ray[3], ray[4], ray[5]}, ray[6], ray[7]);
+    const SampleBuffer buf(samples, samples + n);
+    const StepSchedule sched =
+        sched_kind == 0 ? StepSchedule::constant(dt0) : StepSchedule::linear(dt0, growth);
+    const CompositeResult c = composite_detailed(r, buf, scene, sched);
+    out[0] = c.color.x;
+    out[1] = c.color.y;
+    out[2] = c.color.z;
+    out[3] = c.weight_sum;
+    out[4] = c.transmittance;
+}
+
 } // extern "C"

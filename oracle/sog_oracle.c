@@ -844,3 +844,80 @@ int64_t og_sample_batch(const og_sampler* s, const double* rays, int64_t n,
     }
     return off;
 }
+
+/* ---------------------------------------------------------------------------
+ * compositing consumer (render.hpp)
+ * ------------------------------------------------------------------------- */
+/* Primitive::contains (render.hpp:44-51) */
+static int prim_contains(const og_primitive* q, const double p[3]) {
+    if (q->shape == 0) {
+        const double dx = p[0] - q->center[0], dy = p[1] - q->center[1], dz = p[2] - q->center[2];
+        return dx * dx + dy * dy + dz * dz <= q->radius * q->radius; /* d.dot(d) <= r*r */
+    }
+    return p[0] >= q->lo[0] && p[1] >= q->lo[1] && p[2] >= q->lo[2] && p[0] < q->hi[0] &&
+           p[1] < q->hi[1] && p[2] < q->hi[2];
+}
+
+void og_composite(const double ray[8], const double* samples, int64_t n, const og_primitive* prims,
+                  int32_t n_prims, const double background[3], int32_t sched_kind, double dt0,
+                  double growth, double out[5]) {
+    double c[3] = {0.0, 0.0, 0.0}, ws = 0.0, T = 1.0; /* CompositeResult (render.hpp:91-95) */
+    for (int64_t i = 0; i < n; ++i) {                  /* render.hpp:104-116 */
+        const double t = samples[i];
+        double dt;
+        if (i + 1 < n) {
+            dt = samples[i + 1] - t;
+        } else if (sched_kind == OG_LINEAR) { /* StepSchedule::step (sampling.hpp:36-38) */
+            const double g = growth * t;
+            dt = (dt0 < g) ? g : dt0;
+        } else {
+            dt = dt0;
+        }
+        double p[3];
+        for (int a = 0; a < 3; ++a) p[a] = ray[a] + ray[3 + a] * t; /* Ray::at (ray.hpp:35) */
+        double sigma = 0.0; /* density_at (render.hpp:72-77) */
+        for (int32_t k = 0; k < n_prims; ++k)
+            if (prim_contains(&prims[k], p)) sigma += prims[k].density;
+        if (sigma <= 0.0) continue;
+        const double alpha = 1.0 - exp(-sigma * dt);
+        const double w = T * alpha;
+        double e[3] = {0.0, 0.0, 0.0}, s2 = 0.0; /* emission_at (render.hpp:80-90) */
+        for (int32_t k = 0; k < n_prims; ++k)
+            if (prim_contains(&prims[k], p)) {
+                for (int a = 0; a < 3; ++a) e[a] += prims[k].color[a] * prims[k].density;
+                s2 += prims[k].density;
+            }
+        for (int a = 0; a < 3; ++a) {
+            const double em = s2 > 0.0 ? e[a] / s2 : e[a];
+            c[a] += em * w;
+        }
+        ws += w;
+        T *= 1.0 - alpha;
+    }
+    for (int a = 0; a < 3; ++a) c[a] += background[a] * T; /* render.hpp:117 */
+    out[0] = c[0];
+    out[1] = c[1];
+    out[2] = c[2];
+    out[3] = ws;
+    out[4] = T;
+}
+
+void og_set_pixel(const double rgb[3], uint8_t out[3]) { /* render.hpp:133-139 */
+    for (int a = 0; a < 3; ++a) {
+        const double lo = (0.0 < rgb[a]) ? rgb[a] : 0.0; /* std::max(0.0, v) */
+        const double v = (lo < 1.0) ? lo : 1.0;          /* std::min(1.0, .) */
+        out[a] = (uint8_t)lround(v * 255.0);
+    }
+}
+
+double og_psnr(const uint8_t* a, const uint8_t* b, int64_t n) { /* render.hpp:168-182 */
+    double sq = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double d = (double)a[i] - (double)b[i];
+        sq += d * d;
+    }
+    if (sq == 0.0) return 99.0;
+    const double mse = sq / (double)n;
+    const double v = 10.0 * log10(255.0 * 255.0 / mse);
+    return v < 99.0 ? v : 99.0;
+}

@@ -89,6 +89,26 @@ int64_t og_sample_batch(const og_sampler* s, const double* rays, int64_t n,
                         double* t_starts, double* t_ends, int32_t* ray_indices, uint32_t* cells,
                         uint8_t* levels, int32_t* counters, uint8_t* status);
 
+/* compositing (render.hpp) ------------------------------------------------ */
+typedef struct { /* sog::Primitive (render.hpp:19-56); same layout as sogk_primitive */
+    int32_t shape; /* 0 sphere, 1 box */
+    double center[3];
+    double radius;
+    double lo[3], hi[3];
+    double density;
+    double color[3];
+} og_primitive;
+
+/* composite_detailed (render.hpp:97-118): out[5] = color rgb, weight_sum, transmittance.
+ * sched_kind / dt0 / growth: the StepSchedule of the last sample's step. */
+void og_composite(const double ray[8], const double* samples, int64_t n, const og_primitive* prims,
+                  int32_t n_prims, const double background[3], int32_t sched_kind, double dt0,
+                  double growth, double out[5]);
+/* Image::set_pixel (render.hpp:133-139) of a linear color */
+void og_set_pixel(const double rgb[3], uint8_t out[3]);
+/* psnr (render.hpp:168-182) of two 8-bit buffers of n bytes (99 = identical) */
+double og_psnr(const uint8_t* a, const uint8_t* b, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

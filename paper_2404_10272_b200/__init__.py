@@ -89,6 +89,12 @@ class _Camera(C.Structure):
                 ("height", C.c_int32)]
 
 
+class _Primitive(C.Structure):  # sogk_primitive = sog::Primitive (render.hpp:19-56)
+    _fields_ = [("shape", C.c_int32), ("center", C.c_double * 3), ("radius", C.c_double),
+                ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("density", C.c_double),
+                ("color", C.c_double * 3)]
+
+
 _vp, _i64, _i32, _dbl, _u64 = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_uint64
 _SIGS = {
     "sogk_version": (C.c_char_p, []),
@@ -116,6 +122,11 @@ _SIGS = {
     "sogk_camera_setup": (C.c_int, [_vp, _vp, _vp, _dbl, _i32, _i32, _dbl, C.POINTER(_Camera)]),
     "sogk_camera_rays": (C.c_int, [C.POINTER(_Camera), _i64, _i64, _vp, _vp]),
     "sogk_camera_rays_host": (C.c_int, [C.POINTER(_Camera), _i64, _i64, _vp]),
+    "sogk_scene_analytic": (C.c_int, [C.c_int, C.POINTER(_Transform), _u64, _i32, _vp, _i32, C.POINTER(_i32), _vp]),
+    "sogk_scene_create": (C.c_int, [_vp, _i32, _vp, C.POINTER(_vp)]),
+    "sogk_scene_destroy": (C.c_int, [_vp]),
+    "sogk_composite": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "sogk_render_camera": (C.c_int, [_vp, _vp, C.POINTER(_Camera), _i64, _i64, _vp, _vp, _vp, _vp]),
     "sogk_scene_generate": (C.c_int, [C.c_int, C.POINTER(_Transform), _u64, _dbl, _i32, _dbl, _vp, C.POINTER(_dbl)]),
     "sogk_scene_cascade": (C.c_int, [C.c_int, C.POINTER(_Transform), _u64, _dbl, _i32, _dbl, _i32, _vp, C.POINTER(_Transform)]),
     "sogk_probe_rays": (C.c_int, [C.POINTER(_Transform), _i64, _u64, _vp]),
@@ -717,3 +728,136 @@ def random_blocky_grid(t: GridTransform, seed: int, block_fraction: float,
     _check(lib.sogk_random_blocky_grid(C.byref(tc), seed, block_fraction, noise_fraction,
                                        _ptr(bits)), "random_blocky_grid")
     return bits
+
+
+# ---------------------------------------------------------------------------
+# compositing consumer (render.hpp)
+# ---------------------------------------------------------------------------
+SPHERE, BOX = 0, 1
+
+
+@dataclass
+class Primitive:
+    """sog::Primitive (render.hpp:19-56)."""
+
+    shape: int = SPHERE
+    center: tuple = (0.0, 0.0, 0.0)
+    radius: float = 0.0
+    lo: tuple = (0.0, 0.0, 0.0)
+    hi: tuple = (0.0, 0.0, 0.0)
+    density: float = 0.0
+    color: tuple = (1.0, 1.0, 1.0)
+
+    @staticmethod
+    def sphere(c, r, sigma, rgb) -> "Primitive":
+        return Primitive(SPHERE, tuple(c), float(r), (0.0,) * 3, (0.0,) * 3, float(sigma), tuple(rgb))
+
+    @staticmethod
+    def box(lo, hi, sigma, rgb) -> "Primitive":
+        return Primitive(BOX, (0.0,) * 3, 0.0, tuple(lo), tuple(hi), float(sigma), tuple(rgb))
+
+    def _c(self) -> _Primitive:
+        q = _Primitive()
+        q.shape = self.shape
+        q.radius = self.radius
+        q.density = self.density
+        for a in range(3):
+            q.center[a], q.lo[a], q.hi[a], q.color[a] = self.center[a], self.lo[a], self.hi[a], self.color[a]
+        return q
+
+
+class AnalyticScene:
+    """sog::AnalyticScene (render.hpp:58-92), uploaded to HBM (sogk_scene_create)."""
+
+    def __init__(self, primitives: Sequence[Primitive] = (), background=(0.0, 0.0, 0.0)):
+        self.primitives = list(primitives)
+        self.background = tuple(float(x) for x in background)
+        self._h = None
+
+    @property
+    def handle(self) -> int:
+        """The HBM copy (AnalyticScene::validate + upload on first use)."""
+        if self._h is None:
+            arr = (_Primitive * max(1, len(self.primitives)))(*[p._c() for p in self.primitives])
+            bg = np.asarray(self.background, np.float64)
+            h = C.c_void_p()
+            _check(lib.sogk_scene_create(C.cast(arr, C.c_void_p), len(self.primitives), _ptr(bg),
+                                         C.byref(h)), "scene")
+            self._h = h.value
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.sogk_scene_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def analytic_scene(kind, transform: GridTransform, seed: int = 1, count: int = 12) -> AnalyticScene:
+    """generate_scene's AnalyticScene (scene_gen.hpp:94-176) on `transform`."""
+    tc = transform._c()
+    n = C.c_int32(0)
+    _check(lib.sogk_scene_analytic(_kind(kind), C.byref(tc), seed, count, None, 0, C.byref(n), None),
+           "scene_analytic")
+    arr = (_Primitive * max(1, n.value))()
+    bg = np.zeros(3, np.float64)
+    _check(lib.sogk_scene_analytic(_kind(kind), C.byref(tc), seed, count, C.cast(arr, C.c_void_p),
+                                   n.value, C.byref(n), _ptr(bg)), "scene_analytic")
+    prims = [Primitive(q.shape, tuple(q.center), q.radius, tuple(q.lo), tuple(q.hi), q.density,
+                       tuple(q.color)) for q in arr[:n.value]]
+    return AnalyticScene(prims, tuple(bg))
+
+
+@dataclass
+class FrameResult:
+    """render_frame's result (bench.hpp:415-421): image rows top to bottom, HxWx3 uint8."""
+
+    image: np.ndarray
+    lookups: int
+    steps: int
+    samples: int
+    undefined: int = 0
+    result: object = None  # [H*W, 5] color rgb, weight_sum, transmittance (device tensor)
+
+
+def composite(sampler: "Sampler", scene: AnalyticScene, rays, packed_info, t_starts, stream=None):
+    """composite_detailed (render.hpp:97-118) of every ray of a packed batch on the GPU:
+    -> (result [n,5] = rgb, weight_sum, transmittance; rgb8 [n,3] = Image::set_pixel bytes)."""
+    torch = _torch()
+    n = rays.shape[0]
+    res = torch.empty((n, 5), dtype=torch.float64, device=rays.device)
+    rgb = torch.empty((n, 3), dtype=torch.uint8, device=rays.device)
+    _check(lib.sogk_composite(sampler._h, scene.handle, _ptr(rays), n, _ptr(packed_info),
+                              _ptr(t_starts) if t_starts.numel() else None, _ptr(res), _ptr(rgb),
+                              _stream(stream)), "composite")
+    return res, rgb
+
+
+def render_frame(sampler: "Sampler", scene: AnalyticScene, camera: "Camera", stream=None) -> FrameResult:
+    """render_frame (bench.hpp:424-461) as one fused sample + composite kernel per pixel."""
+    torch = _torch()
+    n = camera.width * camera.height
+    res = torch.empty((n, 5), dtype=torch.float64, device="cuda")
+    rgb = torch.empty((n, 3), dtype=torch.uint8, device="cuda")
+    st = torch.zeros(STATS_LEN, dtype=torch.int64, device="cuda")
+    c = camera._c()
+    _check(lib.sogk_render_camera(sampler._h, scene.handle, C.byref(c), 0, n, _ptr(res), _ptr(rgb),
+                                  _ptr(st), _stream(stream)), "render_camera")
+    hs = st.cpu().numpy()
+    img = rgb.cpu().numpy().reshape(camera.height, camera.width, 3)
+    return FrameResult(img, int(hs[STAT_ANALYZER_LOOKUPS] + hs[STAT_KERNEL_LOOKUPS]),
+                       int(hs[STAT_ANALYZER_STEPS]), int(hs[STAT_TOTAL_SAMPLES]),
+                       int(hs[STAT_UNDEFINED_RAYS]), res)
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    """psnr (render.hpp:168-182) of two equally sized 8-bit images; 99 = identical."""
+    if a.shape != b.shape:
+        raise ValueError("psnr: image dimensions differ")
+    d = a.astype(np.float64) - b.astype(np.float64)
+    sq = float((d * d).sum())
+    if sq == 0.0:
+        return 99.0
+    return min(99.0, 10.0 * math.log10(255.0 * 255.0 / (sq / d.size)))

@@ -919,6 +919,77 @@ int sogk_sample_write_camera(sogk_sampler* s, const sogk_camera* cam, int64_t fi
                       d_t_ends, d_ray_indices, d_cells, d_levels, stream);
 }
 
+// ---- compositing consumer ------------------------------------------------
+struct sogk_scene {
+    SceneDev dev{};
+    sogk_primitive* d_prims = nullptr;
+    ~sogk_scene() { cudaFree(d_prims); }
+};
+
+int sogk_scene_create(const sogk_primitive* h_prims, int32_t n, const double background[3],
+                      sogk_scene** out) {
+    if (!out || n < 0 || (n > 0 && !h_prims) || !background)
+        return fail(SOGK_INVALID_ARG, "sogk_scene_create: NULL argument or negative count");
+    for (int32_t i = 0; i < n; ++i) { // AnalyticScene::validate (render.hpp:62-70)
+        const sogk_primitive& p = h_prims[i];
+        if (p.shape != SOGK_SPHERE && p.shape != SOGK_BOX)
+            return fail(SOGK_INVALID_ARG, "primitive shape must be sphere or box");
+        if (p.density < 0.0) return fail(SOGK_INVALID_ARG, "primitive density must be >= 0");
+        for (int c = 0; c < 3; ++c)
+            if (p.color[c] < 0.0 || p.color[c] > 1.0)
+                return fail(SOGK_INVALID_ARG, "primitive color must lie in [0,1]");
+    }
+    auto* sc = new sogk_scene;
+    if (n > 0) {
+        cudaError_t e = cudaMalloc(&sc->d_prims, size_t(n) * sizeof(sogk_primitive));
+        if (e == cudaSuccess)
+            e = cudaMemcpy(sc->d_prims, h_prims, size_t(n) * sizeof(sogk_primitive), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            delete sc;
+            return cuda_fail(e, "scene upload");
+        }
+    }
+    sc->dev.prims = sc->d_prims;
+    sc->dev.n = n;
+    for (int a = 0; a < 3; ++a) sc->dev.bg[a] = background[a];
+    *out = sc;
+    return SOGK_OK;
+}
+
+int sogk_scene_destroy(sogk_scene* scene) {
+    delete scene;
+    return SOGK_OK;
+}
+
+int sogk_composite(const sogk_sampler* s, const sogk_scene* scene, const double* d_rays, int64_t n,
+                   const int64_t* d_packed_info, const double* d_t_starts, double* d_result,
+                   uint8_t* d_rgb8, void* stream) {
+    if (!s || !scene) return fail(SOGK_INVALID_ARG, "sampler or scene is NULL");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (n == 0) return SOGK_OK;
+    if (!d_rays || !d_packed_info || (!d_result && !d_rgb8))
+        return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    CK(launch_composite(s->v, s->dev, scene->dev, d_rays, n, d_packed_info, d_t_starts, d_result,
+                        d_rgb8, S(stream)),
+       "composite launch");
+    return SOGK_OK;
+}
+
+int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_camera* cam,
+                       int64_t first_pixel, int64_t n, double* d_result, uint8_t* d_rgb8,
+                       int64_t* d_stats, void* stream) {
+    if (!s || !scene) return fail(SOGK_INVALID_ARG, "sampler or scene is NULL");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (!camera_range_ok(cam, first_pixel, n)) return fail(SOGK_INVALID_ARG, "pixel outside image");
+    if (d_stats) CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
+    if (n == 0) return SOGK_OK;
+    if (!d_result && !d_rgb8) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    CK(launch_render(s->v, s->dev, scene->dev, to_dev(*cam), first_pixel, n, d_stats, d_result,
+                     d_rgb8, S(stream)),
+       "render launch");
+    return SOGK_OK;
+}
+
 int sogk_camera_rays(const sogk_camera* cam, int64_t first_pixel, int64_t n, double* d_rays,
                      void* stream) {
     if (!camera_range_ok(cam, first_pixel, n) || (n && !d_rays))

@@ -41,6 +41,19 @@ cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* ra
                          const CameraDev* cam, int64_t first, int64_t n, const int64_t* packed,
                          const SlabDev* slab, int64_t base, double* ts, double* te, int32_t* ri,
                          uint32_t* ce, uint8_t* lv, cudaStream_t st);
+// compositing consumer (sogk_render.cu)
+struct SceneDev { // sog::AnalyticScene in HBM
+    const sogk_primitive* prims;
+    int n;
+    double bg[3];
+};
+cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
+                             const double* rays, int64_t n, const int64_t* packed, const double* ts,
+                             double* result, uint8_t* rgb8, cudaStream_t st);
+cudaError_t launch_render(const Variant& v, const SamplerDev& s, const SceneDev& sc,
+                          const CameraDev& cam, int64_t first, int64_t n, int64_t* stats,
+                          double* result, uint8_t* rgb8, cudaStream_t st);
+
 cudaError_t launch_raygen(const CameraDev& cam, int64_t first, int64_t n, double* rays,
                           cudaStream_t st);
 

@@ -18,6 +18,7 @@
 
 #include "sogk_device.cuh"
 #include "sogk_internal.h"
+#include "sogk_sources.cuh"
 
 namespace sogk {
 
@@ -29,60 +30,6 @@ constexpr int kWriteBlock = 128;
 #ifndef SOGK_COUNT_MINB
 #define SOGK_COUNT_MINB 1 // pass-1 min resident blocks per SM (register cap), A/B-tunable
 #endif
-
-// ---------------------------------------------------------------------------
-// ray sources
-// ---------------------------------------------------------------------------
-struct RaysFromBuffer {
-    const double* rays;
-    __device__ __forceinline__ Ray load(int64_t i) const {
-        const double2* p = reinterpret_cast<const double2*>(rays + 8 * i);
-        const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3);
-        Ray r;
-        r.o[0] = a.x;
-        r.o[1] = a.y;
-        r.o[2] = b.x;
-        r.d[0] = b.y;
-        r.d[1] = c.x;
-        r.d[2] = c.y;
-        r.tmin = d.x;
-        r.tmax = d.y;
-        return r;
-    }
-};
-
-// Camera::pixel_ray, camera.hpp:167-179 (per-camera terms precomputed on the host)
-__device__ __forceinline__ Ray pixel_ray(const CameraDev& c, int64_t pix) {
-    const int px = (int)(pix % c.width);
-    const int py = (int)(pix / c.width);
-    const double u = (((double)px + 0.5) / (double)c.width * 2.0 - 1.0) * c.tan_half * c.aspect;
-    const double v = (1.0 - ((double)py + 0.5) / (double)c.height * 2.0) * c.tan_half;
-    double d[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) d[a] = c.forward[a] + c.right[a] * u + c.cam_up[a] * v;
-    const double len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    Ray r;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        r.o[a] = c.position[a];
-        r.d[a] = d[a] / len;
-    }
-    r.tmin = 0.0;
-    r.tmax = c.t_far;
-    return r;
-}
-
-struct RaysFromCamera {
-    CameraDev cam;
-    int64_t first;
-    __device__ __forceinline__ Ray load(int64_t i) const { return pixel_ray(cam, first + i); }
-};
-
-template <int AN, bool CASC>
-struct PickAn {
-    using Sub = typename std::conditional<AN == SOGK_HDDA, HddaAn, DdaAn>::type;
-    using type = AnyAn<Sub, CASC>;
-};
 
 // ---------------------------------------------------------------------------
 // warp / block scans
@@ -689,29 +636,6 @@ struct Launch {
         return cudaGetLastError();
     }
 };
-
-#define SOGK_DISPATCH(FN, ...)                                                                    \
-    do {                                                                                          \
-        const int key = (v.analyzer << 3) | (v.cascade << 2) | (v.branch << 1) | v.linear;       \
-        switch (key) {                                                                            \
-            case 0: return L::template FN<0, false, false, 0>(__VA_ARGS__);                       \
-            case 1: return L::template FN<0, false, false, 1>(__VA_ARGS__);                       \
-            case 2: return L::template FN<0, false, true, 0>(__VA_ARGS__);                        \
-            case 3: return L::template FN<0, false, true, 1>(__VA_ARGS__);                        \
-            case 4: return L::template FN<0, true, false, 0>(__VA_ARGS__);                        \
-            case 5: return L::template FN<0, true, false, 1>(__VA_ARGS__);                        \
-            case 6: return L::template FN<0, true, true, 0>(__VA_ARGS__);                         \
-            case 7: return L::template FN<0, true, true, 1>(__VA_ARGS__);                         \
-            case 8: return L::template FN<1, false, false, 0>(__VA_ARGS__);                       \
-            case 9: return L::template FN<1, false, false, 1>(__VA_ARGS__);                       \
-            case 10: return L::template FN<1, false, true, 0>(__VA_ARGS__);                       \
-            case 11: return L::template FN<1, false, true, 1>(__VA_ARGS__);                       \
-            case 12: return L::template FN<1, true, false, 0>(__VA_ARGS__);                       \
-            case 13: return L::template FN<1, true, false, 1>(__VA_ARGS__);                       \
-            case 14: return L::template FN<1, true, true, 0>(__VA_ARGS__);                        \
-            default: return L::template FN<1, true, true, 1>(__VA_ARGS__);                        \
-        }                                                                                         \
-    } while (0)
 
 // Variant key: analyzer (0 dda / 1 hdda), cascade, kernel == branch, schedule == linear.
 cudaError_t launch_count(const Variant& v, const SamplerDev& s, const double* rays,

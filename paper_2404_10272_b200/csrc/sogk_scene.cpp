@@ -77,6 +77,7 @@ struct Prim { // Primitive (render.hpp:19-55)
     double radius;
     V3 lo, hi;
     double density;
+    V3 color;
     bool contains(V3 p) const {
         if (sphere) {
             const V3 d = sub(p, center);
@@ -132,8 +133,9 @@ bool make_prims(int kind, const Xform& t, int count, std::mt19937_64& rng, std::
                     c[a] = uniform(rng, wmin[a] + 0.15 * extent[a], wmax[a] - 0.15 * extent[a]);
                 const double r = uniform(rng, 0.04, 0.10) * min_extent;
                 const double sigma = uniform(rng, 4.0, 12.0) / min_extent;
-                for (int k = 0; k < 3; ++k) (void)uniform(rng, 0.1, 1.0); // rgb draws
-                out.push_back(Prim{true, c, r, {}, {}, sigma});
+                V3 rgb;
+                for (int k = 0; k < 3; ++k) rgb[k] = uniform(rng, 0.1, 1.0);
+                out.push_back(Prim{true, c, r, {}, {}, sigma, rgb});
             }
             return true;
         case SOGK_SHELL: {
@@ -147,7 +149,8 @@ bool make_prims(int kind, const Xform& t, int count, std::mt19937_64& rng, std::
                 const double phi = golden * i;
                 const V3 dir{r * std::cos(phi), y, r * std::sin(phi)};
                 const V3 c = add(center, mul(dir, shell_radius));
-                out.push_back(Prim{true, c, bump, {}, {}, 8.0 / min_extent});
+                const V3 rgb = add(V3{0.5, 0.5, 0.5}, mul(dir, 0.45));
+                out.push_back(Prim{true, c, bump, {}, {}, 8.0 / min_extent, rgb});
             }
             return true;
         }
@@ -161,6 +164,8 @@ bool make_prims(int kind, const Xform& t, int count, std::mt19937_64& rng, std::
             auto plane = [&](int axis, int i) { return lo[axis] + (hi[axis] - lo[axis]) * i / cells; };
             for (int axis = 0; axis < 3; ++axis) {
                 const int u = (axis + 1) % 3, v = (axis + 2) % 3;
+                V3 col{0.15, 0.15, 0.15};
+                col[axis] = 0.9;
                 for (int i = 0; i <= cells; ++i)
                     for (int j = 0; j <= cells; ++j) {
                         V3 blo{0, 0, 0}, bhi{0, 0, 0};
@@ -170,13 +175,13 @@ bool make_prims(int kind, const Xform& t, int count, std::mt19937_64& rng, std::
                         bhi[u] = plane(u, i) + w;
                         blo[v] = plane(v, j) - w;
                         bhi[v] = plane(v, j) + w;
-                        out.push_back(Prim{false, {}, 0.0, blo, bhi, sigma});
+                        out.push_back(Prim{false, {}, 0.0, blo, bhi, sigma, col});
                     }
             }
             return true;
         }
         default:
-            out.push_back(Prim{false, {}, 0.0, wmin, wmax, 3.0 / min_extent});
+            out.push_back(Prim{false, {}, 0.0, wmin, wmax, 3.0 / min_extent, {0.7, 0.7, 0.7}});
             return false;
     }
 }
@@ -217,6 +222,39 @@ int sogk_scene_generate(int kind, const sogk_transform* tr, uint64_t seed, doubl
         uint64_t n = 0;
         for (uint64_t i = 0; i < t.count(); ++i) n += (h_bits[i >> 3] >> (i & 7)) & 1u;
         *occupancy = double(n) / double(t.count());
+    }
+    return SOGK_OK;
+}
+
+int sogk_scene_analytic(int kind, const sogk_transform* tr, uint64_t seed, int32_t count,
+                        sogk_primitive* h_prims, int32_t cap, int32_t* n_prims,
+                        double background[3]) {
+    if (!valid_transform(tr) || !n_prims || kind < 0 || kind > 3 || count < 1)
+        return SOGK_INVALID_ARG;
+    const Xform t(*tr);
+    std::mt19937_64 rng(seed);
+    std::vector<Prim> prims;
+    make_prims(kind, t, count, rng, prims);
+    *n_prims = int32_t(prims.size());
+    if (background) { // scene.background (scene_gen.hpp:112)
+        background[0] = 0.05;
+        background[1] = 0.06;
+        background[2] = 0.08;
+    }
+    if (!h_prims) return SOGK_OK; // size query
+    if (cap < int32_t(prims.size())) return SOGK_INSUFFICIENT_CAPACITY;
+    for (size_t i = 0; i < prims.size(); ++i) {
+        const Prim& p = prims[i];
+        sogk_primitive& q = h_prims[i];
+        q.shape = p.sphere ? SOGK_SPHERE : SOGK_BOX;
+        for (int a = 0; a < 3; ++a) {
+            q.center[a] = p.center[a];
+            q.lo[a] = p.lo[a];
+            q.hi[a] = p.hi[a];
+            q.color[a] = p.color[a];
+        }
+        q.radius = p.radius;
+        q.density = p.density;
     }
     return SOGK_OK;
 }

@@ -107,7 +107,39 @@ class Oracle:
         L.og_sample_batch.restype = C.c_int64
         L.og_sample_batch.argtypes = [C.POINTER(_OgSampler), _dp, C.c_int64, C.c_int64,
                                       C.c_int64, _i64p, _dp, _dp, _i32p, _u32p, _u8p, _i32p, _u8p]
+        L.og_composite.argtypes = [_dp, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, _dp,
+                                   C.c_int32, C.c_double, C.c_double, _dp]
+        L.og_set_pixel.argtypes = [_dp, _u8p]
+        L.og_psnr.restype = C.c_double
+        L.og_psnr.argtypes = [_u8p, _u8p, C.c_int64]
         self._owned = []
+
+    # compositing (render.hpp) --------------------------------------------------
+    @staticmethod
+    def _prims(prims) -> np.ndarray:
+        """Primitives as the og_primitive layout (int32 shape + pad, then 14 doubles)."""
+        dt = np.dtype([("shape", np.int32), ("pad", np.int32), ("center", np.float64, 3),
+                       ("radius", np.float64), ("lo", np.float64, 3), ("hi", np.float64, 3),
+                       ("density", np.float64), ("color", np.float64, 3)])
+        a = np.zeros(max(1, len(prims)), dt)
+        for i, p in enumerate(prims):
+            a[i] = (p.shape, 0, p.center, p.radius, p.lo, p.hi, p.density, p.color)
+        return a
+
+    def composite(self, ray, samples, prims, background, sched_kind, dt0, growth=0.0) -> np.ndarray:
+        """composite_detailed (render.hpp:97-118) -> [r, g, b, weight_sum, transmittance]."""
+        out = np.zeros(5, np.float64)
+        smp = np.ascontiguousarray(samples, np.float64)
+        pa = self._prims(prims)
+        self.L.og_composite(np.ascontiguousarray(ray, np.float64), smp.ctypes.data if smp.size else None,
+                            smp.size, pa.ctypes.data, len(prims), np.asarray(background, np.float64),
+                            sched_kind, dt0, growth, out)
+        return out
+
+    def set_pixel(self, rgb) -> np.ndarray:
+        out = np.zeros(3, np.uint8)
+        self.L.og_set_pixel(np.asarray(rgb, np.float64), out)
+        return out
 
     # grids ----------------------------------------------------------------
     def dense(self, g: Grid) -> int:
@@ -215,6 +247,14 @@ class RefLib:
                                        _i64p, _dp, _dp, _u32p, _u8p, _i32p]
         L.ref_collect_events.restype = C.c_int64
         L.ref_collect_events.argtypes = [C.c_void_p, _dp, C.c_int64, _i32p, _dp, _i64p]
+        L.ref_scene_primitives.restype = C.c_int
+        L.ref_scene_primitives.argtypes = [C.c_int, _i32p, _dp, C.c_double, C.c_uint64, C.c_double,
+                                           C.c_int, _dp, C.c_int, _dp]
+        L.ref_render_frame.argtypes = [C.c_int, C.c_uint64, C.c_double, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _u8p,
+                                       _i64p]
+        L.ref_composite.argtypes = [_dp, C.c_void_p, C.c_int64, _dp, C.c_int, _dp, C.c_int,
+                                    C.c_double, C.c_double, _dp]
         L.ref_time_sampler.restype = C.c_double
         L.ref_time_sampler.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_void_p, C.c_int, C.c_int,
                                        C.POINTER(C.c_int64)]
@@ -242,6 +282,37 @@ class RefLib:
                                  fraction, count, threshold, levels, bits, wm, vx)
         return [Grid(tuple(int(x) for x in r), tuple(wm[3 * b:3 * b + 3]), float(vx[b]),
                      bits[b * nb:(b + 1) * nb].copy()) for b in range(levels)]
+
+    def scene_primitives(self, kind, res=128, seed=1, fraction=0.05, count=12,
+                         wmin=(-1.0, -1.0, -1.0), extent=2.0):
+        """generate_scene's AnalyticScene -> (array [n, 16], background[3])."""
+        r = np.array([res] * 3, np.int32)
+        out = np.zeros((512, 16), np.float64)
+        bg = np.zeros(3, np.float64)
+        n = self.L.ref_scene_primitives(SCENE_KINDS[kind], r, np.asarray(wmin, np.float64),
+                                        extent / res, seed, fraction, count, out, 512, bg)
+        return out[:n].copy(), bg
+
+    def composite(self, ray, samples, prims16, background, sched_kind, dt0, growth=0.0):
+        """the reference's composite_detailed; prims16 as returned by scene_primitives."""
+        out = np.zeros(5, np.float64)
+        smp = np.ascontiguousarray(samples, np.float64)
+        pa = np.ascontiguousarray(prims16, np.float64).reshape(-1, 16)
+        self.L.ref_composite(np.ascontiguousarray(ray, np.float64), smp.ctypes.data if smp.size else None,
+                             smp.size, pa if pa.size else np.zeros(16), len(pa),
+                             np.asarray(background, np.float64), sched_kind, dt0, growth, out)
+        return out
+
+    def render_frame(self, kind, seed=1, fraction=0.0, resolution=128, cascades=1, sched_kind=0,
+                     width=160, height=120, grid=0, analyzer=0, kernel=0, threads=0):
+        """render_frame (bench.hpp:424-461) of one variant on build_assets(cfg) ->
+        (image HxWx3 uint8, lookups, steps, samples)."""
+        rgb = np.zeros(width * height * 3, np.uint8)
+        st = np.zeros(3, np.int64)
+        nt = threads or max(1, self.L.ref_hardware_concurrency())
+        self.L.ref_render_frame(SCENE_KINDS[kind], seed, fraction, resolution, cascades, sched_kind,
+                                width, height, grid, analyzer, kernel, nt, rgb, st)
+        return rgb.reshape(height, width, 3), int(st[0]), int(st[1]), int(st[2])
 
     def camera_rays(self, pos=(1.9, 1.4, 2.3), target=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0),
                     vfov=42.0, width=160, height=120, t_far=1e6) -> np.ndarray:
