@@ -132,18 +132,21 @@ class Workload:
             self.objects = []
             for kind, kw in CFG2_OBJECTS:
                 bits, occ = P.generate_scene(kind, base, **kw)
-                self.objects.append(dict(label=f"{kind}:{kw}", levels=[(base, bits)], occupancy=occ))
+                self.objects.append(dict(label=f"{kind}:{kw}", levels=[(base, bits)], occupancy=occ,
+                                         scene=(kind, kw.get("seed", 1), kw.get("count", 12), base)))
             self.width = self.height = 800
             self.desc = ("8 procedural 128^3 objects (shell s1, shell s2 n256, blobs s1..s4 n6..48, "
                          "sponge s1, random 2%), 800x800 orbit views, dt0 = half voxel")
         elif name == "cfg1":
             bits, occ = P.generate_scene("shell", base, seed=1)
-            self.objects = [dict(label="shell s1", levels=[(base, bits)], occupancy=occ)]
+            self.objects = [dict(label="shell s1", levels=[(base, bits)], occupancy=occ,
+                                 scene=("shell", 1, 12, base))]
             self.width = self.height = 800
             self.desc = "single-level 128^3 shell s1, 800x800 bench camera, dt0 = half voxel"
         elif name == "cfg3":
             lv = P.build_dense_cascade("blobs", base, 4, seed=1)
-            self.objects = [dict(label="blobs s1 x4 cascade", levels=lv, occupancy=None)]
+            self.objects = [dict(label="blobs s1 x4 cascade", levels=lv, occupancy=None,
+                                 scene=("blobs", 1, 12, base))]
             self.cascade = True
             self.width, self.height = 1297, 840
             self.schedule = P.StepSchedule.linear(0.5 * base.voxel_size, 1.0 / 256.0)
@@ -157,6 +160,15 @@ class Workload:
             self.desc = "512^3 blobs s1 (1.44%), 2^24 make_probe_rays, dt0 = half voxel"
         else:
             raise SystemExit(f"unknown config {name}")
+
+    def camera(self, step_index: int, obj: int, rank: int, world: int):
+        """The camera of (global step, object) for this rank (None for probe-ray configs)."""
+        if self.name == "cfg4":
+            return None
+        view = view_of(step_index, rank, world, N_VIEWS, obj * (N_VIEWS // max(1, len(self.objects))))
+        if self.name in ("cfg1", "cfg3"):
+            view = 0
+        return orbit_camera(self.P, view, self.width, self.height)
 
     def rays_per_object(self) -> int:
         return self.n_probe if self.name == "cfg4" else self.width * self.height
@@ -325,6 +337,40 @@ def run_gpu(args):
         results[vname] = dict(ms=ms, count_ms=count_ms, write_ms=write_ms, samples=samples,
                               hit_rays=nhit, clocks=clk.summary())
 
+    # --- render leg: render_frame fused (sample + composite per pixel, no sample arrays),
+    # the paper's rendered-frames metric; one frame = one object's view
+    render = None
+    if not args.no_render and wl.name != "cfg4":
+        scenes = [P.analytic_scene(o["scene"][0], o["scene"][3], seed=o["scene"][1], count=o["scene"][2])
+                  for o in wl.objects]
+        npx = wl.width * wl.height
+        r_res = torch.empty((npx, 5), dtype=torch.float64, device=dev)
+        r_rgb = torch.empty((npx, 3), dtype=torch.uint8, device=dev)
+        r_st = torch.zeros(8, dtype=torch.int64, device=dev)
+        render = {}
+        for vname, smp in samplers.items():
+            def rstep(s_):
+                for o in range(n_obj):
+                    cam = wl.camera(s_, o, rank, world)._c()
+                    P._check(P.lib.sogk_render_camera(smp[o]._h, scenes[o].handle, P.C.byref(cam), 0, npx,
+                                                      r_res.data_ptr(), r_rgb.data_ptr(), r_st.data_ptr(),
+                                                      stream.cuda_stream or None), "render")
+            for s_ in range(args.warmup):
+                rstep(s_)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for k in range(args.steps):
+                rstep(args.warmup + k)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            rms = e0.elapsed_time(e1)
+            frames = args.steps * n_obj
+            render[vname] = {"frames_per_sec": frames / (rms / 1e3), "ms_per_frame": rms / frames,
+                             "mpix_per_sec": frames * npx / (rms / 1e3) / 1e6}
+
     # --- e2e through the host C-ABI entry point (pinned host buffers, H2D/D2H timed)
     e2e = None
     if not args.no_e2e:
@@ -473,7 +519,11 @@ def run_gpu(args):
                           "basis": "N_rays*(64+16) + N_samples*24 + VDB bytes (SURVEY §8d)"},
         "vdb_build_ms": build_ms,
         "grid_bytes": {"dense": dense_bytes, "vdb_sog1": vdb_bytes},
-        "gpu_launches": 4 * launches,  # count, scan, expand, tail per object
+        "render": ({"what": "render_frame fused on the GPU (Camera::pixel_ray -> sampling -> "
+                             "composite_detailed -> Image::set_pixel per pixel, no sample arrays), "
+                             f"{wl.width}x{wl.height} frames, rank 0",
+                     "variants": render} if render else None),
+        "gpu_launches": 4 * launches,  # count, scan, gather, tail per object
         "clocks": h["clocks"],
     }
     if e2e:
@@ -611,6 +661,7 @@ def main():
     ap.add_argument("--cpu-stride", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = {"cfg1": 200, "cfg2": 50, "cfg3": 200, "cfg4": 10}[args.config]

@@ -167,11 +167,28 @@ struct sogk_sampler {
     // sogk_sample_host scratch
     void* hb = nullptr;
     size_t hb_bytes = 0;
+    // sogk_render_camera scratch: stats (256 B) | packed counts [n][2]
+    void* rb = nullptr;
+    size_t rb_bytes = 0;
 
     ~sogk_sampler() {
         cudaFree(ws);
         cudaFree(hb);
+        cudaFree(rb);
     }
+    int ensure_render(int64_t n) {
+        const size_t need = size_t(n) * 16 + 256;
+        if (need > rb_bytes) {
+            cudaFree(rb);
+            rb = nullptr;
+            rb_bytes = 0;
+            CK(cudaMalloc(&rb, need), "render scratch");
+            rb_bytes = need;
+        }
+        return SOGK_OK;
+    }
+    int64_t* render_stats() const { return static_cast<int64_t*>(rb); }
+    int64_t* render_packed() const { return reinterpret_cast<int64_t*>(static_cast<char*>(rb) + 256); }
 
     // pass 1 -> pass 2 handshake: the sample slabs of the last count call
     const void* last_rays = nullptr;
@@ -836,7 +853,7 @@ static CameraDev to_dev(const sogk_camera& c) {
 
 static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* cam,
                       int64_t first, int64_t n, int64_t* d_packed, int64_t* d_stats,
-                      uint8_t* d_status, int32_t* d_counters, void* stream) {
+                      uint8_t* d_status, int32_t* d_counters, void* stream, bool scan = true) {
     if (!s) return fail(SOGK_INVALID_ARG, "sampler is NULL");
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
     if (!d_stats) return fail(SOGK_INVALID_ARG, "stats buffer is NULL");
@@ -854,9 +871,10 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
                     d_status, d_counters, slab, S(stream)),
        "count launch");
-    CK(launch_scan(n, d_packed, d_stats, s->tiles(),
-                   reinterpret_cast<unsigned int*>(s->tiles() + tiles), S(stream)),
-       "scan launch");
+    if (scan)
+        CK(launch_scan(n, d_packed, d_stats, s->tiles(),
+                       reinterpret_cast<unsigned int*>(s->tiles() + tiles), S(stream)),
+           "scan launch");
     s->last_rays = cam ? nullptr : d_rays;
     s->last_cam = cam != nullptr;
     s->last_first = first;
@@ -981,11 +999,17 @@ int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_came
     if (!s || !scene) return fail(SOGK_INVALID_ARG, "sampler or scene is NULL");
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
     if (!camera_range_ok(cam, first_pixel, n)) return fail(SOGK_INVALID_ARG, "pixel outside image");
-    if (d_stats) CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
-    if (n == 0) return SOGK_OK;
     if (!d_result && !d_rgb8) return fail(SOGK_INVALID_ARG, "NULL device buffer");
-    CK(launch_render(s->v, s->dev, scene->dev, to_dev(*cam), first_pixel, n, d_stats, d_result,
-                     d_rgb8, S(stream)),
+    int st = s->ensure_render(n);
+    if (st) return st;
+    int64_t* stats = d_stats ? d_stats : s->render_stats();
+    // pass 1 on the camera rays: counts, counters, samples into the slabs (no scan needed)
+    st = count_impl(s, nullptr, cam, first_pixel, n, s->render_packed(), stats, nullptr, nullptr,
+                    stream, /*scan=*/false);
+    if (st) return st;
+    if (n == 0) return SOGK_OK;
+    CK(launch_render_composite(s->v, s->dev, scene->dev, to_dev(*cam), first_pixel, n,
+                               s->render_packed(), s->slab(n), d_result, d_rgb8, S(stream)),
        "render launch");
     return SOGK_OK;
 }

@@ -50,9 +50,11 @@ struct SceneDev { // sog::AnalyticScene in HBM
 cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
                              const double* rays, int64_t n, const int64_t* packed, const double* ts,
                              double* result, uint8_t* rgb8, cudaStream_t st);
-cudaError_t launch_render(const Variant& v, const SamplerDev& s, const SceneDev& sc,
-                          const CameraDev& cam, int64_t first, int64_t n, int64_t* stats,
-                          double* result, uint8_t* rgb8, cudaStream_t st);
+// after launch_count on the camera rays: composite every ray from its slab (+ overflow tail)
+cudaError_t launch_render_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
+                                    const CameraDev& cam, int64_t first, int64_t n,
+                                    const int64_t* packed, const SlabDev& S, double* result,
+                                    uint8_t* rgb8, cudaStream_t st);
 
 cudaError_t launch_raygen(const CameraDev& cam, int64_t first, int64_t n, double* rays,
                           cudaStream_t st);

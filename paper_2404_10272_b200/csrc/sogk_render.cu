@@ -2,9 +2,13 @@
 //
 // composite_kernel: composite_detailed (render.hpp:97-118) for every ray of a packed batch,
 //   one thread per ray over its contiguous samples.
-// render_kernel:    render_frame's per-pixel work (bench.hpp:424-461) fused: the pixel's ray
-//   is generated (Camera::pixel_ray), sampled with pass 1's loop and composited sample by
-//   sample in registers; no sample ever reaches HBM.
+// render (sogk_render_camera): render_frame's per-pixel work (bench.hpp:424-461) as
+//   pass 1 (count_kernel on camera rays, samples into the per-ray slabs) followed by
+//   composite_slab_kernel, which composites each ray straight from its slab row: no scan, no
+//   packed sample arrays.  Shading (a loop over every primitive per sample) dominates; done
+//   in its own kernel the lanes of a warp shade in step, where interleaving it with the
+//   divergent traversal loop measured 4x slower.  Rays whose samples overflowed the slab are
+//   finished by render_tail_kernel (slab part, then the resumed traversal, composited).
 //
 // FP64 with the reference's operation order (Ray::at, density/emission sums in primitive
 // order, Vec3 operators); exp() is CUDA's (≤ 1 ulp), not glibc's, so results match the CPU
@@ -118,77 +122,61 @@ __global__ void __launch_bounds__(kRenderBlock)
     comp.store(r, result, rgb8);
 }
 
+// composite from the slabs of pass 1 (rays whose samples all fit: count <= C)
+template <int SCH, class Src>
+__global__ void __launch_bounds__(kRenderBlock)
+    composite_slab_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const Src src,
+                          int64_t n, const int64_t* __restrict__ packed, const SlabDev S,
+                          double* __restrict__ result, uint8_t* __restrict__ rgb8) {
+    const int64_t r = (int64_t)blockIdx.x * kRenderBlock + threadIdx.x;
+    if (r >= n) return;
+    const long long cnt = __ldg(reinterpret_cast<const longlong2*>(packed) + r).y;
+    if (cnt > S.C) return; // render_tail_kernel
+    const Ray ray = src.load(r);
+    Compositor<SCH> comp;
+    comp.init();
+    const double* row = S.t + r * S.C;
+    for (long long k = 0; k < cnt; ++k) comp.add(sc, ray, s, __ldg(row + k));
+    comp.finish(sc, ray, s);
+    comp.store(r, result, rgb8);
+}
+
+// rays whose samples overflowed the slab: the slab part, then the traversal resumed at
+// the first event that did not fit, all composited in order
 template <int AN, bool CASC, bool BR, int SCH, class Src>
 __global__ void __launch_bounds__(kRenderBlock)
-    render_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const Src src, int64_t n,
-                  int64_t* __restrict__ stats, double* __restrict__ result,
-                  uint8_t* __restrict__ rgb8) {
-    const int64_t r = (int64_t)blockIdx.x * kRenderBlock + threadIdx.x;
-    long long smp = 0, lk = 0, sp = 0, klk = 0, und = 0;
-    if (r < n) {
+    render_tail_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const Src src,
+                       const int64_t* __restrict__ packed, const SlabDev S,
+                       double* __restrict__ result, uint8_t* __restrict__ rgb8) {
+    const unsigned cnt = *S.ovf_ctr;
+    for (unsigned i = blockIdx.x * kRenderBlock + threadIdx.x; i < cnt; i += gridDim.x * kRenderBlock) {
+        const int64_t r = S.ovf_list[i];
+        const long long total = __ldg(reinterpret_cast<const longlong2*>(packed) + r).y;
+        Resume res = S.resume[r];
+        const long long fill = res.tag >> 8;
+        res.tag &= 255;
         const Ray ray = src.load(r);
         Compositor<SCH> comp;
         comp.init();
-        if (ray_valid(ray)) {
-            RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
-            gen.init(ray, s);
-            for (;;) { // pass 1's loop, the samples go to the compositor
-                Event ev;
-                double t_last0;
-                const int st = gen.step_event(s, ev, t_last0);
-                if (st == 0) break;
-                if (st == 1) continue;
-                double t = gen.t_last;
-                int k = 0;
-                bool stuck = false;
-                while (t <= ev.t1) { // while (t <= t1) { push(t); t += step(t); }
-                    comp.add(sc, ray, s, t);
-                    const double tn = t + ladder_step<SCH>(t, s.dt0, s.growth);
-                    ++k;
-                    if (!(tn > t)) { // t + step == t: the reference loops forever
-                        stuck = true;
-                        break;
-                    }
-                    t = tn;
-                }
-                gen.t_last = t;
-                if (stuck) {
-                    gen.stalled = true;
-                    break;
-                }
-                if (BR) gen.kernel_lookups += k;
-                smp += k;
-            }
-            if (gen.undefined()) { // the reference never returns: no samples, like pass 1
-                comp.init();
-                smp = 0;
-                und = 1;
-            } else {
-                lk = gen.an.lookups();
-                sp = gen.an.steps();
-                klk = gen.kernel_lookups;
+        const double* row = S.t + r * S.C;
+        for (long long k = 0; k < fill; ++k) comp.add(sc, ray, s, row[k]);
+        RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
+        gen.init(ray, s);
+        gen.resume(s, res);
+        long long done = fill;
+        Run run;
+        while (done < total) {
+            const int st = gen.step(s, run);
+            if (st == 0) break;
+            if (st != 2) continue;
+            double t = run.first;
+            for (int k = 0; k < run.n && done < total; ++k, ++done) {
+                comp.add(sc, ray, s, t);
+                t = t + ladder_step<SCH>(t, s.dt0, s.growth);
             }
         }
         comp.finish(sc, ray, s);
         comp.store(r, result, rgb8);
-    }
-    if (stats) { // warp-level reduction, one atomic per warp and counter
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            smp += __shfl_xor_sync(0xffffffffu, smp, o);
-            lk += __shfl_xor_sync(0xffffffffu, lk, o);
-            sp += __shfl_xor_sync(0xffffffffu, sp, o);
-            klk += __shfl_xor_sync(0xffffffffu, klk, o);
-            und += __shfl_xor_sync(0xffffffffu, und, o);
-        }
-        if ((threadIdx.x & 31) == 0) {
-            unsigned long long* S = reinterpret_cast<unsigned long long*>(stats);
-            if (smp) atomicAdd(S + SOGK_STAT_TOTAL_SAMPLES, (unsigned long long)smp);
-            if (lk) atomicAdd(S + SOGK_STAT_ANALYZER_LOOKUPS, (unsigned long long)lk);
-            if (sp) atomicAdd(S + SOGK_STAT_ANALYZER_STEPS, (unsigned long long)sp);
-            if (klk) atomicAdd(S + SOGK_STAT_KERNEL_LOOKUPS, (unsigned long long)klk);
-            if (und) atomicAdd(S + SOGK_STAT_UNDEFINED_RAYS, (unsigned long long)und);
-        }
     }
 }
 
@@ -205,22 +193,30 @@ cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneD
 
 struct RenderLaunch {
     template <int AN, bool CASC, bool BR, int SCH>
-    static cudaError_t render(const SamplerDev& s, const SceneDev& sc, const RaysFromCamera& src,
-                              int64_t n, int64_t* stats, double* result, uint8_t* rgb8,
-                              cudaStream_t st) {
-        const unsigned blocks = (unsigned)((n + kRenderBlock - 1) / kRenderBlock);
-        render_kernel<AN, CASC, BR, SCH, RaysFromCamera>
-            <<<blocks, kRenderBlock, 0, st>>>(s, sc, src, n, stats, result, rgb8);
+    static cudaError_t tail(const SamplerDev& s, const SceneDev& sc, const RaysFromCamera& src,
+                            const int64_t* packed, const SlabDev& S, double* result, uint8_t* rgb8,
+                            unsigned grid, cudaStream_t st) {
+        render_tail_kernel<AN, CASC, BR, SCH, RaysFromCamera>
+            <<<grid, kRenderBlock, 0, st>>>(s, sc, src, packed, S, result, rgb8);
         return cudaGetLastError();
     }
 };
 
-cudaError_t launch_render(const Variant& v, const SamplerDev& s, const SceneDev& sc,
-                          const CameraDev& cam, int64_t first, int64_t n, int64_t* stats,
-                          double* result, uint8_t* rgb8, cudaStream_t st) {
-    using L = RenderLaunch;
+cudaError_t launch_render_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
+                                    const CameraDev& cam, int64_t first, int64_t n,
+                                    const int64_t* packed, const SlabDev& S, double* result,
+                                    uint8_t* rgb8, cudaStream_t st) {
     const RaysFromCamera src{cam, first};
-    SOGK_DISPATCH(render, s, sc, src, n, stats, result, rgb8, st);
+    const unsigned blocks = (unsigned)((n + kRenderBlock - 1) / kRenderBlock);
+    if (v.linear)
+        composite_slab_kernel<1, RaysFromCamera><<<blocks, kRenderBlock, 0, st>>>(s, sc, src, n, packed, S, result, rgb8);
+    else
+        composite_slab_kernel<0, RaysFromCamera><<<blocks, kRenderBlock, 0, st>>>(s, sc, src, n, packed, S, result, rgb8);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const unsigned tg = blocks < 148u * 8u ? (blocks ? blocks : 1u) : 148u * 8u;
+    using L = RenderLaunch;
+    SOGK_DISPATCH(tail, s, sc, src, packed, S, result, rgb8, tg, st);
 }
 
 } // namespace sogk

@@ -97,7 +97,7 @@ __device__ __forceinline__ void store_resume(Resume* dst, const Run& run, int fi
 // pass 1: per-ray counts, status, counters, resume state
 // ---------------------------------------------------------------------------
 struct Stats5 {
-    long long inv = 0, und = 0, lk = 0, sp = 0, klk = 0, ovf = 0;
+    long long inv = 0, und = 0, lk = 0, sp = 0, klk = 0, ovf = 0, smp = 0;
     __device__ __forceinline__ void flush(int64_t* stats) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -107,6 +107,7 @@ struct Stats5 {
             sp += __shfl_xor_sync(0xffffffffu, sp, o);
             klk += __shfl_xor_sync(0xffffffffu, klk, o);
             ovf += __shfl_xor_sync(0xffffffffu, ovf, o);
+            smp += __shfl_xor_sync(0xffffffffu, smp, o);
         }
         if ((threadIdx.x & 31) == 0) {
             unsigned long long* S = reinterpret_cast<unsigned long long*>(stats);
@@ -116,6 +117,8 @@ struct Stats5 {
             if (sp) atomicAdd(S + SOGK_STAT_ANALYZER_STEPS, (unsigned long long)sp);
             if (klk) atomicAdd(S + SOGK_STAT_KERNEL_LOOKUPS, (unsigned long long)klk);
             if (ovf) atomicAdd(S + SOGK_STAT_SLAB_OVERFLOW_RAYS, (unsigned long long)ovf);
+            // the scan (when it runs) overwrites the total with the same value
+            if (smp) atomicAdd(S + SOGK_STAT_TOTAL_SAMPLES, (unsigned long long)smp);
         }
     }
 };
@@ -142,6 +145,7 @@ __device__ __forceinline__ void count_finish(const Gen& gen, long long r, long l
         counters[3 * r + 2] = klk;
     }
     reinterpret_cast<longlong2*>(packed)[r] = make_longlong2(0, cnt);
+    acc.smp += cnt;
     acc.lk += lk;
     acc.sp += sp;
     acc.klk += klk;
