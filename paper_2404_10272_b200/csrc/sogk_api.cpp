@@ -941,8 +941,63 @@ int sogk_sample_write_camera(sogk_sampler* s, const sogk_camera* cam, int64_t fi
 struct sogk_scene {
     SceneDev dev{};
     sogk_primitive* d_prims = nullptr;
-    ~sogk_scene() { cudaFree(d_prims); }
+    int* d_grid = nullptr;
+    ~sogk_scene() {
+        cudaFree(d_prims);
+        cudaFree(d_grid);
+    }
 };
+
+// Candidate grid (SceneDev): a cube of kCells^3 cells around the union of the primitive
+// bounding boxes; a primitive is listed in every cell its box (grown by one cell on each
+// side, far above rounding in Primitive::contains) touches.
+static void build_candidate_grid(const sogk_primitive* p, int32_t n, SceneDev& d,
+                                 std::vector<int>& cstart, std::vector<int>& cand) {
+    d.gres = 0;
+    if (n < 4) return; // a loop over a few primitives is as cheap as the lookup
+    double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    auto box = [&](const sogk_primitive& q, double* b0, double* b1) {
+        for (int a = 0; a < 3; ++a) {
+            b0[a] = q.shape == SOGK_SPHERE ? q.center[a] - q.radius : q.lo[a];
+            b1[a] = q.shape == SOGK_SPHERE ? q.center[a] + q.radius : q.hi[a];
+        }
+    };
+    for (int32_t i = 0; i < n; ++i) {
+        double b0[3], b1[3];
+        box(p[i], b0, b1);
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], b0[a]);
+            hi[a] = std::max(hi[a], b1[a]);
+        }
+    }
+    double ext = 0.0;
+    for (int a = 0; a < 3; ++a) ext = std::max(ext, hi[a] - lo[a]);
+    if (!(ext > 0.0) || !std::isfinite(ext)) return;
+    constexpr int kCells = 32;
+    const double cell = ext / kCells;
+    d.gres = kCells;
+    d.ginv = 1.0 / cell;
+    for (int a = 0; a < 3; ++a) d.glo[a] = lo[a];
+    std::vector<std::vector<int>> lists(size_t(kCells) * kCells * kCells);
+    for (int32_t i = 0; i < n; ++i) {
+        double b0[3], b1[3];
+        box(p[i], b0, b1);
+        int c0[3], c1[3];
+        for (int a = 0; a < 3; ++a) {
+            c0[a] = std::max(0, int(std::floor((b0[a] - lo[a]) / cell)) - 1);
+            c1[a] = std::min(kCells - 1, int(std::floor((b1[a] - lo[a]) / cell)) + 1);
+        }
+        for (int z = c0[2]; z <= c1[2]; ++z)
+            for (int y = c0[1]; y <= c1[1]; ++y)
+                for (int x = c0[0]; x <= c1[0]; ++x)
+                    lists[(size_t(z) * kCells + y) * kCells + x].push_back(i); // ascending i
+    }
+    cstart.assign(lists.size() + 1, 0);
+    for (size_t c = 0; c < lists.size(); ++c) cstart[c + 1] = cstart[c] + int(lists[c].size());
+    cand.clear();
+    cand.reserve(size_t(cstart.back()));
+    for (const auto& l : lists) cand.insert(cand.end(), l.begin(), l.end());
+}
 
 int sogk_scene_create(const sogk_primitive* h_prims, int32_t n, const double background[3],
                       sogk_scene** out) {
@@ -970,6 +1025,23 @@ int sogk_scene_create(const sogk_primitive* h_prims, int32_t n, const double bac
     sc->dev.prims = sc->d_prims;
     sc->dev.n = n;
     for (int a = 0; a < 3; ++a) sc->dev.bg[a] = background[a];
+    std::vector<int> cstart, cand;
+    build_candidate_grid(h_prims, n, sc->dev, cstart, cand);
+    if (sc->dev.gres > 0) {
+        const size_t nb = (cstart.size() + cand.size()) * sizeof(int);
+        cudaError_t e = cudaMalloc(&sc->d_grid, nb);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(sc->d_grid, cstart.data(), cstart.size() * sizeof(int), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && !cand.empty())
+            e = cudaMemcpy(sc->d_grid + cstart.size(), cand.data(), cand.size() * sizeof(int),
+                           cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            delete sc;
+            return cuda_fail(e, "scene grid upload");
+        }
+        sc->dev.cstart = sc->d_grid;
+        sc->dev.cand = sc->d_grid + cstart.size();
+    }
     *out = sc;
     return SOGK_OK;
 }

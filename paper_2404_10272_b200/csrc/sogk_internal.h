@@ -46,6 +46,15 @@ struct SceneDev { // sog::AnalyticScene in HBM
     const sogk_primitive* prims;
     int n;
     double bg[3];
+    // candidate grid over the primitives' bounding boxes: the primitives that may contain a
+    // point of cell c are cand[cstart[c] .. cstart[c+1]) in increasing index order (every
+    // box grown by one cell), so density/emission sums visit the same primitives in the
+    // same order as the reference's full loop
+    int gres;           // cells per axis (0: no grid, loop over all primitives)
+    double glo[3];      // grid origin
+    double ginv;        // 1 / cell size
+    const int* cstart;  // [gres^3 + 1]
+    const int* cand;
 };
 cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
                              const double* rays, int64_t n, const int64_t* packed, const double* ts,

@@ -23,22 +23,42 @@ namespace sogk {
 
 constexpr int kRenderBlock = 128;
 
+__device__ __forceinline__ bool prim_contains(const sogk_primitive& q, const double p[3]) {
+    if (q.shape == SOGK_SPHERE) { // Primitive::contains (render.hpp:44-51)
+        const double dx = p[0] - q.center[0], dy = p[1] - q.center[1], dz = p[2] - q.center[2];
+        return dx * dx + dy * dy + dz * dz <= q.radius * q.radius;
+    }
+    return p[0] >= q.lo[0] && p[1] >= q.lo[1] && p[2] >= q.lo[2] && p[0] < q.hi[0] &&
+           p[1] < q.hi[1] && p[2] < q.hi[2];
+}
+
 // AnalyticScene::density_at / emission_at (render.hpp:72-91) at p, one pass over the
-// primitives in order (both sums run in the same order as the reference's two loops)
+// primitives in order (both sums run in the same order as the reference's two loops).
+// With the candidate grid only the primitives listed for p's cell are tested: every other
+// primitive's (grown) box misses the cell, so it cannot contain p, and the list keeps
+// index order -- the sums are the reference's.
 __device__ __forceinline__ double scene_at(const SceneDev& sc, const double p[3], double e[3]) {
     double sigma = 0.0;
     e[0] = e[1] = e[2] = 0.0;
-    for (int i = 0; i < sc.n; ++i) {
-        const sogk_primitive& q = sc.prims[i]; // warp-uniform: one broadcast per field
-        bool in;
-        if (q.shape == SOGK_SPHERE) { // Primitive::contains (render.hpp:44-51)
-            const double dx = p[0] - q.center[0], dy = p[1] - q.center[1], dz = p[2] - q.center[2];
-            in = dx * dx + dy * dy + dz * dz <= q.radius * q.radius;
-        } else {
-            in = p[0] >= q.lo[0] && p[1] >= q.lo[1] && p[2] >= q.lo[2] && p[0] < q.hi[0] &&
-                 p[1] < q.hi[1] && p[2] < q.hi[2];
+    int i0 = 0, i1 = sc.n;
+    const int* list = nullptr;
+    if (sc.gres > 0) {
+        int c[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double g = (p[a] - sc.glo[a]) * sc.ginv;
+            if (!(g > -1.0 && g < (double)(sc.gres + 1))) return 0.0; // outside every box
+            const int ci = (int)floor(g);
+            c[a] = ci < 0 ? 0 : (ci >= sc.gres ? sc.gres - 1 : ci);
         }
-        if (in) {
+        const int cell = (c[2] * sc.gres + c[1]) * sc.gres + c[0];
+        i0 = __ldg(sc.cstart + cell);
+        i1 = __ldg(sc.cstart + cell + 1);
+        list = sc.cand;
+    }
+    for (int k = i0; k < i1; ++k) {
+        const sogk_primitive& q = sc.prims[list ? __ldg(list + k) : k];
+        if (prim_contains(q, p)) {
             e[0] += q.color[0] * q.density;
             e[1] += q.color[1] * q.density;
             e[2] += q.color[2] * q.density;
