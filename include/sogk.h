@@ -64,10 +64,10 @@ enum {
     SOGK_RAY_UNDEFINED = 2  /* reference HddaTraversal::next never returns (traversal.hpp:238-241) */
 };
 
-typedef enum { SOGK_DDA = 0, SOGK_HDDA = 1 } sogk_analyzer;       /* bench.hpp:27 AnalyzerKind */
+typedef enum { SOGK_DDA = 0, SOGK_HDDA = 1, SOGK_CD = 2 } sogk_analyzer; /* bench.hpp:27 AnalyzerKind */
 typedef enum { SOGK_BRANCH = 0, SOGK_SKIP = 1 } sogk_kernel;       /* sampling.hpp:155 KernelKind */
 typedef enum { SOGK_CONSTANT = 0, SOGK_LINEAR = 1 } sogk_schedule; /* sampling.hpp:18-39 */
-typedef enum { SOGK_GRID_DENSE = 0, SOGK_GRID_VDB = 1 } sogk_grid_kind;
+typedef enum { SOGK_GRID_DENSE = 0, SOGK_GRID_VDB = 1, SOGK_GRID_DISTANCE = 2 } sogk_grid_kind;
 typedef enum { SOGK_BLOBS = 0, SOGK_SHELL = 1, SOGK_SPONGE = 2, SOGK_RANDOM = 3 } sogk_scene_kind;
 
 /* stats block written by sogk_sample_count (int64[SOGK_STATS_LEN], device) */
@@ -144,6 +144,13 @@ int sogk_grid_create_dense_device(const sogk_transform* t, const uint8_t* d_bits
                                   void* stream, sogk_grid** out);
 /* build_sparse (sparse.hpp:333-371) on the GPU: ballot/popc masks + prefix-scan leaf slots */
 int sogk_grid_build_vdb(const sogk_grid* dense, void* stream, sogk_grid** out);
+/* build_distance (distance.hpp:45-103): the chessboard distance field of a dense grid
+ * (int32 per voxel in HBM), the grid the CD analyzer (CdTraversal, traversal.hpp:270-337)
+ * marches.  Exact, so equal to the reference's chamfer values. */
+int sogk_grid_build_distance(const sogk_grid* dense, void* stream, sogk_grid** out);
+/* DistanceGrid payload (int32 per voxel, x fastest) to the host; *all_empty = all_empty() */
+int sogk_grid_download_distance(const sogk_grid* g, int32_t* h_dist, size_t count,
+                                int32_t* all_empty);
 /* deserialize_dense / deserialize_sparse (io.hpp:143-151, 183-214) straight to HBM */
 int sogk_grid_load_sog0(const uint8_t* bytes, size_t len, void* stream, sogk_grid** out);
 int sogk_grid_load_sog1(const uint8_t* bytes, size_t len, void* stream, sogk_grid** out);

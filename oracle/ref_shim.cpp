@@ -35,8 +35,9 @@ namespace {
 struct RefSampler {
     DenseCascade dense;
     SparseCascade sparse;
+    DistanceCascade distance;
     int cascade = 0;
-    int analyzer = 0; // 0 dda, 1 hdda
+    int analyzer = 0; // 0 dda, 1 hdda, 2 cd
     KernelKind kernel = KernelKind::skip;
     StepSchedule sched;
 };
@@ -112,6 +113,9 @@ void sample_one(const RefSampler& s, const Ray& ray, RayOut& out) {
         if (s.analyzer == 0) {
             Recording<DdaTraversal> an(s.dense.levels[0], ray);
             run_recorded(an, s, [&] { return DenseProbe{&s.dense.levels[0]}; }, out);
+        } else if (s.analyzer == 2) { // run_sampler(ray, dense, dist, ...) (sampling.hpp:198-212)
+            Recording<CdTraversal> an(s.distance.levels[0], ray);
+            run_recorded(an, s, [&] { return DenseProbe{&s.dense.levels[0]}; }, out);
         } else {
             Recording<HddaTraversal> an(s.sparse.levels[0], ray);
             run_recorded(an, s, [&] { return SparseProbe(s.sparse.levels[0]); }, out);
@@ -120,6 +124,9 @@ void sample_one(const RefSampler& s, const Ray& ray, RayOut& out) {
         if (s.analyzer == 0) {
             Recording<CascadeTraversal<DenseGrid>> an(s.dense, ray);
             run_recorded(an, s, [&] { return CascadeProbe<DenseGrid>(s.dense); }, out);
+        } else if (s.analyzer == 2) {
+            Recording<CascadeTraversal<DistanceGrid>> an(s.distance, ray);
+            run_recorded(an, s, [&] { return CascadeProbe<DistanceGrid>(s.distance); }, out);
         } else {
             Recording<CascadeTraversal<SparseGrid>> an(s.sparse, ray);
             run_recorded(an, s, [&] { return CascadeProbe<SparseGrid>(s.sparse); }, out);
@@ -133,9 +140,12 @@ std::size_t sample_plain(const RefSampler& s, const Ray& ray) {
     const bool cascade = s.cascade || s.dense.levels.size() > 1;
     if (!cascade) {
         if (s.analyzer == 0) return run_sampler(ray, s.dense.levels[0], s.kernel, s.sched).samples.size();
+        if (s.analyzer == 2)
+            return run_sampler(ray, s.dense.levels[0], s.distance.levels[0], s.kernel, s.sched).samples.size();
         return run_sampler(ray, s.sparse.levels[0], s.kernel, s.sched).samples.size();
     }
     if (s.analyzer == 0) return run_cascade_sampler(ray, s.dense, s.kernel, s.sched).samples.size();
+    if (s.analyzer == 2) return run_cascade_sampler(ray, s.distance, s.kernel, s.sched).samples.size();
     return run_cascade_sampler(ray, s.sparse, s.kernel, s.sched).samples.size();
 }
 
@@ -301,6 +311,8 @@ void* ref_sampler_create(int n_levels, int cascade, const int32_t res[3], const 
     }
     if (analyzer == 1)
         for (const auto& d : s->dense.levels) s->sparse.levels.push_back(build_sparse(d));
+    if (analyzer == 2)
+        for (const auto& d : s->dense.levels) s->distance.levels.push_back(build_distance(d));
     s->cascade = cascade;
     s->analyzer = analyzer;
     s->kernel = kernel == 0 ? KernelKind::branch : KernelKind::skip;
@@ -374,12 +386,18 @@ int64_t ref_collect_events(void* h, const double* ray, int64_t cap, int32_t* ev_
         if (s.analyzer == 0) {
             DdaTraversal an(s.dense.levels[0], r);
             drain(an);
+        } else if (s.analyzer == 2) {
+            CdTraversal an(s.distance.levels[0], r);
+            drain(an);
         } else {
             HddaTraversal an(s.sparse.levels[0], r);
             drain(an);
         }
     } else if (s.analyzer == 0) {
         CascadeTraversal<DenseGrid> an(s.dense, r);
+        drain(an);
+    } else if (s.analyzer == 2) {
+        CascadeTraversal<DistanceGrid> an(s.distance, r);
         drain(an);
     } else {
         CascadeTraversal<SparseGrid> an(s.sparse, r);
@@ -497,6 +515,20 @@ void ref_composite(const double* ray, const double* samples, int64_t n, const do
     out[2] = c.color.z;
     out[3] = c.weight_sum;
     out[4] = c.transmittance;
+}
+
+// build_distance (distance.hpp:45-103): int32 per voxel; returns all_empty()
+int ref_build_distance(const int32_t res[3], const double wmin[3], double voxel, const uint8_t* bits,
+                       int32_t* out) {
+    DenseGrid d(make_transform(res, wmin, voxel));
+    std::memcpy(d.payload().data(), bits, d.payload().size());
+    const DistanceGrid g = build_distance(d);
+    const Vec3i r = g.transform().resolution;
+    int64_t i = 0;
+    for (int z = 0; z < r.z; ++z)
+        for (int y = 0; y < r.y; ++y)
+            for (int x = 0; x < r.x; ++x) out[i++] = g.at({x, y, z});
+    return g.all_empty() ? 1 : 0;
 }
 
 } // extern "C"

@@ -41,6 +41,9 @@ struct og_grid {
     int32_t* slots;      /* [nodes][4096] */
     uint8_t* leaves;     /* [leaves][64] */
     int64_t n_nodes, n_leaves;
+    /* distance (DistanceGrid, distance.hpp:15-43): int32 per voxel, x fastest */
+    int32_t* dist;
+    int32_t all_empty;
 };
 
 /* ------------------------------------------------------------------------ */
@@ -99,7 +102,82 @@ void og_grid_free(og_grid* g) {
     free(g->kinds);
     free(g->slots);
     free(g->leaves);
+    free(g->dist);
     free(g);
+}
+
+/* build_distance, distance.hpp:45-103: two-pass chamfer over the 26-neighbourhood with unit
+ * weights (exact for the chessboard metric), sentinel max(resolution) when nothing is occupied */
+og_grid* og_distance_build(const og_grid* d) {
+    if (!d || d->sparse || d->dist) return NULL;
+    og_grid* g = (og_grid*)calloc(1, sizeof(og_grid));
+    for (int a = 0; a < 3; ++a) {
+        g->res[a] = d->res[a];
+        g->wmin[a] = d->wmin[a];
+    }
+    g->voxel = d->voxel;
+    const int rx = d->res[0], ry = d->res[1], rz = d->res[2];
+    const int64_t n = (int64_t)rx * ry * rz;
+    g->dist = (int32_t*)malloc((size_t)n * sizeof(int32_t));
+    const int32_t kInf = 1 << 29;
+    int any = 0;
+    int64_t idx = 0;
+    for (int z = 0; z < rz; ++z)
+        for (int y = 0; y < ry; ++y)
+            for (int x = 0; x < rx; ++x, ++idx) {
+                const int ijk[3] = {x, y, z};
+                const int occ = dense_bit(d, ijk);
+                g->dist[idx] = occ ? 0 : kInf;
+                any |= occ;
+            }
+    if (!any) {
+        int32_t sentinel = rx > ry ? rx : ry;
+        if (rz > sentinel) sentinel = rz;
+        for (int64_t i = 0; i < n; ++i) g->dist[i] = sentinel;
+        g->all_empty = 1;
+        return g;
+    }
+#define DAT(X, Y, Z) (((X) < 0 || (Y) < 0 || (Z) < 0 || (X) >= rx || (Y) >= ry || (Z) >= rz) \
+                          ? kInf : g->dist[((int64_t)(Z) * ry + (Y)) * rx + (X)])
+#define MIN1(b, v) do { const int32_t v_ = (v) + 1; if (v_ < (b)) (b) = v_; } while (0)
+    for (int z = 0; z < rz; ++z) /* forward: neighbours lexicographically before (dz, dy, dx) */
+        for (int y = 0; y < ry; ++y)
+            for (int x = 0; x < rx; ++x) {
+                int32_t best = DAT(x, y, z);
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) MIN1(best, DAT(x + dx, y + dy, z - 1));
+                MIN1(best, DAT(x - 1, y - 1, z));
+                MIN1(best, DAT(x, y - 1, z));
+                MIN1(best, DAT(x + 1, y - 1, z));
+                MIN1(best, DAT(x - 1, y, z));
+                g->dist[((int64_t)z * ry + y) * rx + x] = best;
+            }
+    for (int z = rz - 1; z >= 0; --z) /* backward: the mirror image */
+        for (int y = ry - 1; y >= 0; --y)
+            for (int x = rx - 1; x >= 0; --x) {
+                int32_t best = DAT(x, y, z);
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) MIN1(best, DAT(x + dx, y + dy, z + 1));
+                MIN1(best, DAT(x + 1, y + 1, z));
+                MIN1(best, DAT(x, y + 1, z));
+                MIN1(best, DAT(x - 1, y + 1, z));
+                MIN1(best, DAT(x + 1, y, z));
+                g->dist[((int64_t)z * ry + y) * rx + x] = best;
+            }
+#undef DAT
+#undef MIN1
+    return g;
+}
+
+const int32_t* og_distance_data(const og_grid* g, int32_t* all_empty) {
+    if (all_empty) *all_empty = g ? g->all_empty : 0;
+    return g ? g->dist : NULL;
+}
+
+/* DistanceGrid::at (distance.hpp:27-30): out of bounds reads 1 */
+static inline int32_t dist_at(const og_grid* g, const int ijk[3]) {
+    if (!contains(g, ijk)) return 1;
+    return g->dist[((int64_t)ijk[2] * g->res[1] + ijk[1]) * g->res[0] + ijk[0]];
 }
 
 /* read_leaf_block, sparse.hpp:283-324.  Both the aligned fast path and the
@@ -436,7 +514,7 @@ static inline int argmin_axis(const double t[3]) { /* traversal.hpp:107-112 */
 /* ------------------------------------------------------------------------ */
 typedef struct {
     const og_grid* grid;
-    int hdda;
+    int hdda; /* 0 DDA, 1 HDDA, 2 CD */
     og_geom geom;
     int ijk[3];
     int next_plane[3];
@@ -461,7 +539,7 @@ static void an_init(og_an* an, const og_grid* grid, int hdda, const og_ray* r, i
     }
     entry_cell(&an->geom, grid->res, an->ijk);
     an->t_cur = an->geom.t_enter;
-    if (hdda) return;
+    if (hdda) return; /* HDDA and CD derive their planes per step */
     for (int a = 0; a < 3; ++a) {
         if (an->geom.step[a] == 0) {
             an->next_plane[a] = 0;
@@ -566,7 +644,61 @@ static int hdda_next(og_an* an, og_event* ev) { /* HddaTraversal::next :213-248 
     }
 }
 
-static int an_next(og_an* an, og_event* ev) { return an->hdda ? hdda_next(an, ev) : dda_next(an, ev); }
+static int cd_next(og_an* an, og_event* ev) { /* CdTraversal::next, traversal.hpp:290-327 */
+    if (an->done) return 0;
+    int degenerate = 0;
+    for (;;) {
+        const int32_t d = dist_at(an->grid, an->ijk);
+        ++an->lookups;
+        const int half = d > 1 ? d - 1 : 0;
+        int low[3];
+        for (int a = 0; a < 3; ++a) low[a] = an->ijk[a] - half;
+        const int extent = 2 * half + 1;
+        double t_cross[3];
+        for (int a = 0; a < 3; ++a) {
+            if (an->geom.step[a] == 0) {
+                t_cross[a] = KINF;
+            } else {
+                const double plane = an->geom.step[a] > 0 ? (double)(low[a] + extent) : (double)low[a];
+                t_cross[a] = plane_t(&an->geom, a, plane);
+            }
+        }
+        const int axis = argmin_axis(t_cross);
+        const double t1 = t_cross[axis];
+        ev->level = LV_VOXEL;
+        ev->occupied = d == 0;
+        ev->grid_level = 0;
+        for (int a = 0; a < 3; ++a) ev->ijk[a] = low[a];
+        if (t1 >= an->geom.t_exit) {
+            ++an->steps;
+            an->done = 1;
+            ev->t0 = an->t_cur;
+            ev->t1 = an->geom.t_exit;
+            return 1;
+        }
+        const int stepped = an->geom.step[axis] > 0 ? low[axis] + extent : low[axis] - 1;
+        if (t1 <= an->t_cur) { /* degenerate corner crossing (:311-314) */
+            cell_after_crossing(&an->geom, an->t_cur, axis, stepped, an->ijk);
+            /* the same edge-crossing spin as HddaTraversal */
+            if (++degenerate > an->spin_cap) {
+                an->undefined = 1;
+                an->done = 1;
+                return 0;
+            }
+            continue;
+        }
+        ev->t0 = an->t_cur;
+        ev->t1 = t1;
+        ++an->steps;
+        cell_after_crossing(&an->geom, t1, axis, stepped, an->ijk);
+        an->t_cur = t1;
+        return 1;
+    }
+}
+
+static int an_next(og_an* an, og_event* ev) {
+    return an->hdda == 2 ? cd_next(an, ev) : an->hdda ? hdda_next(an, ev) : dda_next(an, ev);
+}
 
 /* ------------------------------------------------------------------------ */
 /* cascades, sampling.hpp:222-415                                            */
@@ -679,7 +811,7 @@ static int cascade_next(og_cascade* c, og_event* ev) { /* :361-392 */
         og_ray sub = c->ray;
         sub.tmin = c->seg_t0[c->seg];
         sub.tmax = c->seg_t1[c->seg];
-        an_init(&c->sub, c->s->levels[c->seg_level[c->seg]], c->s->analyzer == OG_HDDA, &sub,
+        an_init(&c->sub, c->s->levels[c->seg_level[c->seg]], c->s->analyzer, &sub,
                 c->s->spin_cap);
         c->has_sub = 1;
     }
@@ -699,7 +831,7 @@ static void any_init(og_any* x, const og_sampler* s, const og_ray* r) {
     if (x->cascade)
         cascade_init(&x->cas, s, r);
     else
-        an_init(&x->an, s->levels[0], s->analyzer == OG_HDDA, r, s->spin_cap);
+        an_init(&x->an, s->levels[0], s->analyzer, r, s->spin_cap);
 }
 static int any_valid(const og_any* x) { return x->cascade ? x->cas.valid : x->an.geom.valid; }
 static double any_t_enter(const og_any* x) { return x->cascade ? x->cas.t_enter : x->an.geom.t_enter; }
@@ -758,6 +890,9 @@ static int probe(const og_sampler* s, const og_event* ev) {
     if (ev->grid_level < 0) return 0;
     const og_grid* g = s->levels[(s->cascade || s->n_levels > 1) ? ev->grid_level : 0];
     if (s->analyzer == OG_HDDA) return sparse_query(g, ev->ijk).occupied;
+    /* CD: the single-grid kernel probes the dense grid (DenseProbe, sampling.hpp:200-203),
+     * the cascade one the distance level (grid_occupancy, :281); both answer ev.occupied */
+    if (s->analyzer == OG_CD) return dist_at(g, ev->ijk) == 0;
     return dense_bit(g, ev->ijk);
 }
 

@@ -31,7 +31,7 @@ extern "C" {
 typedef struct og_grid og_grid;
 
 /* analyzer / kernel / schedule / status codes (same values as include/sogk.h) */
-enum { OG_DDA = 0, OG_HDDA = 1 };
+enum { OG_DDA = 0, OG_HDDA = 1, OG_CD = 2 };
 enum { OG_BRANCH = 0, OG_SKIP = 1 };
 enum { OG_CONSTANT = 0, OG_LINEAR = 1 };
 enum { OG_RAY_OK = 0, OG_RAY_INVALID = 1, OG_RAY_UNDEFINED = 2 };
@@ -48,7 +48,7 @@ typedef struct {
     const og_grid* levels[8];
     int32_t n_levels;
     int32_t cascade;    /* 1: CascadeTraversal (sampling.hpp:305-415) even for one level */
-    int32_t analyzer;   /* OG_DDA (dense levels) / OG_HDDA (sparse levels) */
+    int32_t analyzer;   /* OG_DDA (dense levels) / OG_HDDA (sparse levels) / OG_CD (distance levels) */
     int32_t kernel;     /* OG_BRANCH / OG_SKIP */
     int32_t sched_kind; /* OG_CONSTANT / OG_LINEAR */
     double dt0, growth;
@@ -59,6 +59,9 @@ typedef struct {
 og_grid* og_dense_create(const int32_t res[3], const double wmin[3], double voxel,
                          const uint8_t* bits);
 og_grid* og_sparse_build(const og_grid* dense);            /* sparse.hpp:333-371 */
+og_grid* og_distance_build(const og_grid* dense);          /* distance.hpp:45-103 */
+/* the distance payload (int32 per voxel, x fastest) and DistanceGrid::all_empty */
+const int32_t* og_distance_data(const og_grid* dist, int32_t* all_empty);
 void og_grid_free(og_grid* g);
 int64_t og_sparse_serialize(const og_grid* sparse, uint8_t* buf, int64_t cap); /* io.hpp:161-181 */
 int64_t og_sparse_leaf_count(const og_grid* sparse);

@@ -105,6 +105,8 @@ _SIGS = {
     "sogk_grid_create_dense": (C.c_int, [C.POINTER(_Transform), _vp, C.c_size_t, _vp, C.POINTER(_vp)]),
     "sogk_grid_create_dense_device": (C.c_int, [C.POINTER(_Transform), _vp, C.c_size_t, _vp, C.POINTER(_vp)]),
     "sogk_grid_build_vdb": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
+    "sogk_grid_build_distance": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
+    "sogk_grid_download_distance": (C.c_int, [_vp, _vp, C.c_size_t, C.POINTER(_i32)]),
     "sogk_grid_load_sog0": (C.c_int, [_vp, C.c_size_t, _vp, C.POINTER(_vp)]),
     "sogk_grid_load_sog1": (C.c_int, [_vp, C.c_size_t, _vp, C.POINTER(_vp)]),
     "sogk_grid_export_sog0": (C.c_int, [_vp, _vp, C.POINTER(C.c_size_t)]),
@@ -327,6 +329,36 @@ def build_sparse(dense: DenseGrid, stream=None) -> SparseGrid:
     return SparseGrid(h.value, dense.transform())
 
 
+class DistanceGrid(_Grid):
+    """sog::DistanceGrid (distance.hpp:15-43): chessboard distance per voxel, in HBM."""
+
+    _kind = 2
+
+    def distances(self) -> np.ndarray:
+        """int32 [z][y][x] (the payload DistanceGrid::at reads in bounds)."""
+        t = self.transform()
+        out = np.empty(t.voxel_count(), np.int32)
+        _check(lib.sogk_grid_download_distance(self._h, _ptr(out), out.size, None), "distance")
+        return out.reshape(t.resolution[2], t.resolution[1], t.resolution[0])
+
+    def all_empty(self) -> bool:
+        ae = C.c_int32(0)
+        _check(lib.sogk_grid_download_distance(self._h, None, 0, C.byref(ae)), "distance")
+        return bool(ae.value)
+
+    def memory_bytes(self) -> int:
+        return int(self.info().memory_bytes)
+
+
+def build_distance(dense: DenseGrid, stream=None) -> DistanceGrid:
+    """build_distance (distance.hpp:45-103) on the GPU (exact separable transform)."""
+    if not isinstance(dense, DenseGrid):
+        raise ValueError("build_distance needs a DenseGrid")
+    h = C.c_void_p()
+    _check(lib.sogk_grid_build_distance(dense._h, _stream(stream), C.byref(h)), "build_distance")
+    return DistanceGrid(h.value, dense.transform())
+
+
 def _export(fn, h) -> bytes:
     n = C.c_size_t(0)
     _check(fn(h, None, C.byref(n)), "export")
@@ -376,7 +408,7 @@ class KernelKind:
 
 
 class Analyzer:
-    dda, hdda = 0, 1
+    dda, hdda, cd = 0, 1, 2
 
 
 @dataclass(frozen=True)

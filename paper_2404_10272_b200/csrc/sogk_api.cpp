@@ -91,6 +91,9 @@ struct sogk_grid {
     uint32_t* region_leaves = nullptr;
     uint32_t* total_leaves = nullptr;
     uint64_t leaf_capacity = 0;
+    // distance
+    int32_t* dist = nullptr;
+    unsigned* dist_any = nullptr; // device flag: some voxel occupied (!all_empty)
     // host-side root map when loaded from SOG1 (entries that do not map to an
     // in-grid aligned region are kept for export only); empty for built grids
     std::vector<RootEntry> extra_entries;
@@ -109,6 +112,8 @@ struct sogk_grid {
         cudaFree(leaves);
         cudaFree(region_leaves);
         cudaFree(total_leaves);
+        cudaFree(dist);
+        cudaFree(dist_any);
     }
 
     GridDev dev() const {
@@ -137,6 +142,7 @@ struct sogk_grid {
         g.value_mask = value_mask;
         g.prefix = prefix;
         g.leaves = leaves;
+        g.dist = dist;
         return g;
     }
 
@@ -371,6 +377,49 @@ int sogk_grid_build_vdb(const sogk_grid* d, void* stream, sogk_grid** out) {
     return SOGK_OK;
 }
 
+int sogk_grid_build_distance(const sogk_grid* d, void* stream, sogk_grid** out) {
+    if (!out) return fail(SOGK_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!d || d->kind != SOGK_GRID_DENSE)
+        return fail(SOGK_INVALID_ARG, "build_distance needs a dense grid");
+    for (int a = 0; a < 3; ++a)
+        if (d->t.res[a] > 2047) return fail(SOGK_INVALID_ARG, "distance lines are limited to 2047 voxels");
+    auto* g = new sogk_grid;
+    g->kind = SOGK_GRID_DISTANCE;
+    g->t = d->t;
+    g->device = d->device;
+    const uint64_t n = voxel_count(d->t);
+    int32_t* scratch = nullptr;
+    cudaError_t e = dalloc(&g->dist, n);
+    if (e == cudaSuccess) e = dalloc(&g->dist_any, 1);
+    if (e == cudaSuccess) e = dalloc(&scratch, n);
+    if (e == cudaSuccess) e = launch_distance_build(d->dev(), g->dist, scratch, g->dist_any, S(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream)); // before the scratch goes
+    cudaFree(scratch);
+    if (e != cudaSuccess) {
+        delete g;
+        return cuda_fail(e, "distance build");
+    }
+    *out = g;
+    return SOGK_OK;
+}
+
+int sogk_grid_download_distance(const sogk_grid* g, int32_t* h_dist, size_t count,
+                                int32_t* all_empty) {
+    if (!g || g->kind != SOGK_GRID_DISTANCE) return fail(SOGK_INVALID_ARG, "not a distance grid");
+    const uint64_t n = voxel_count(g->t);
+    if (h_dist) {
+        if (count < n) return fail(SOGK_INSUFFICIENT_CAPACITY, "buffer smaller than the grid");
+        CK(cudaMemcpy(h_dist, g->dist, n * sizeof(int32_t), cudaMemcpyDeviceToHost), "distance D2H");
+    }
+    if (all_empty) {
+        unsigned any = 0;
+        CK(cudaMemcpy(&any, g->dist_any, sizeof(unsigned), cudaMemcpyDeviceToHost), "flag D2H");
+        *all_empty = any ? 0 : 1;
+    }
+    return SOGK_OK;
+}
+
 int sogk_grid_destroy(sogk_grid* g) {
     delete g;
     return SOGK_OK;
@@ -386,6 +435,11 @@ int sogk_grid_get_info(const sogk_grid* g, sogk_grid_info* out) {
     if (g->kind == SOGK_GRID_DENSE) {
         out->memory_bytes = int64_t(g->nbytes); // io.hpp:223-225
         out->device_bytes = int64_t(g->nbytes);
+        return SOGK_OK;
+    }
+    if (g->kind == SOGK_GRID_DISTANCE) { // variant_memory_bytes: voxel_count * 4 (bench.hpp:468-470)
+        out->memory_bytes = int64_t(voxel_count(g->t)) * 4;
+        out->device_bytes = out->memory_bytes;
         return SOGK_OK;
     }
     int64_t internal = 0;
@@ -764,7 +818,7 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     if (!levels || !desc) return fail(SOGK_INVALID_ARG, "NULL argument");
     if (n_levels < 1) return fail(SOGK_INVALID_ARG, "cascade has no levels");
     if (n_levels > SOGK_MAX_LEVELS) return fail(SOGK_INVALID_ARG, "too many cascade levels");
-    if (desc->analyzer != SOGK_DDA && desc->analyzer != SOGK_HDDA)
+    if (desc->analyzer != SOGK_DDA && desc->analyzer != SOGK_HDDA && desc->analyzer != SOGK_CD)
         return fail(SOGK_INVALID_ARG, "unknown analyzer");
     if (desc->kernel != SOGK_BRANCH && desc->kernel != SOGK_SKIP)
         return fail(SOGK_INVALID_ARG, "unknown kernel");
@@ -774,12 +828,14 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     if (!(desc->dt0 > 0.0)) return fail(SOGK_INVALID_ARG, "step size must be positive");
     if (desc->schedule == SOGK_LINEAR && desc->growth < 0.0)
         return fail(SOGK_INVALID_ARG, "growth must be non-negative");
-    const int want = desc->analyzer == SOGK_DDA ? SOGK_GRID_DENSE : SOGK_GRID_VDB;
+    const int want = desc->analyzer == SOGK_DDA    ? SOGK_GRID_DENSE
+                     : desc->analyzer == SOGK_HDDA ? SOGK_GRID_VDB
+                                                   : SOGK_GRID_DISTANCE;
     for (int b = 0; b < n_levels; ++b) {
         if (!levels[b]) return fail(SOGK_INVALID_ARG, "NULL grid level");
         if (levels[b]->kind != want)
-            return fail(SOGK_INVALID_ARG,
-                        "analyzers are bound to their grid: dda marches dense grids, hdda VDBs");
+            return fail(SOGK_INVALID_ARG, "analyzers are bound to their grid: dda marches dense "
+                                          "grids, hdda VDBs, cd distance grids");
     }
     const bool cascade = desc->cascade || n_levels > 1;
     if (cascade) { // validate_cascade (sampling.hpp:253-273)

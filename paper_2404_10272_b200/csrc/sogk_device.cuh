@@ -10,6 +10,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 #include "sogk_ladder.cuh"
 #include "sogk_layout.h"
@@ -397,8 +398,13 @@ __device__ __forceinline__ HddaGeomSmem& hdda_geom() {
 }
 #endif
 
-struct HddaAn {
-    static constexpr bool kHdda = true;
+// The same loop serves CdTraversal (traversal.hpp:270-337, CD = true): its "node" is the
+// cube of half-width d-1 around the voxel (d = chessboard distance, proven empty), with
+// low corner ijk - (d-1) instead of an extent-aligned VDB node; everything else -- exit
+// planes, argmin, clamp to t_exit, degenerate re-derivation, spin guard -- is identical.
+template <bool CD>
+struct NodeAn {
+    static constexpr bool kHdda = !CD;
 #if SOGK_HDDA_SMEM
     __device__ __forceinline__ double& E(int a) { return hdda_geom().e[a][threadIdx.x]; }
     __device__ __forceinline__ double& DV(int a) { return hdda_geom().dv[a][threadIdx.x]; }
@@ -471,7 +477,19 @@ struct HddaAn {
     // -1 = degenerate iteration consumed (call again).
     __device__ __forceinline__ int next(const GridDev& g, Event& ev) {
         if (done) return 0;
-        const Query q = cur.query(g, ijk);
+        Query q;
+        int half = 0;
+        if constexpr (CD) { // DistanceGrid::at: out of bounds reads 1 (distance.hpp:27-30)
+            const int32_t d = in_bounds(g, ijk)
+                                  ? __ldg(g.dist + ((int64_t)ijk[2] * g.res[1] + ijk[1]) * g.res[0] + ijk[0])
+                                  : 1;
+            half = d > 1 ? d - 1 : 0;
+            q.ext = 2 * half + 1;
+            q.level = LV_VOXEL;
+            q.occ = d == 0;
+        } else {
+            q = cur.query(g, ijk);
+        }
         ++lookups;
         // exit plane of the node on each axis (:218-228), mirrored: lo + ext walking up,
         // -lo walking down; the cell just past it (`stepped`, :236-237) is plane' ^ m
@@ -480,7 +498,7 @@ struct HddaAn {
         int pl[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const int lo = ijk[a] & -q.ext;
+            const int lo = CD ? ijk[a] - half : (ijk[a] & -q.ext);
             ev.ijk[a] = lo;
             pl[a] = (lo ^ M(a)) + (M(a) ? 1 : q.ext);
             tc[a] = te + ((double)pl[a] - E(a)) * IV(a);
@@ -524,7 +542,8 @@ struct HddaAn {
     }
 
     __device__ __forceinline__ bool probe(const GridDev& g, const Event& ev) { // SparseProbe
-        return cur.query(g, ev.ijk).occ;
+        if constexpr (CD) return ev.occ; // DenseProbe at the cube's low corner == (d == 0)
+        else return cur.query(g, ev.ijk).occ;
     }
 
     // Resume at an emitted event: the node origin queries the same node, so
@@ -543,6 +562,9 @@ struct HddaAn {
     __device__ __forceinline__ double enter_t() const { return TE(); }
     __device__ __forceinline__ double exit_t() const { return TX(); }
 };
+
+using HddaAn = NodeAn<false>;
+using CdAn = NodeAn<true>;
 
 // CascadeTraversal<GridT>, sampling.hpp:305-415, over SOGK_MAX_LEVELS levels.
 // Every loop over levels and cuts has a fixed trip count (unrolled, guarded by n_levels)
@@ -729,7 +751,9 @@ struct CascadeAn {
 
     __device__ __forceinline__ bool probe(const SamplerDev& s, const Event& ev) { // CascadeProbe
         if (ev.grid_level < 0) return false;
-        if constexpr (Sub::kHdda) {
+        if constexpr (std::is_same<Sub, CdAn>::value) {
+            return ev.occ;
+        } else if constexpr (Sub::kHdda) {
             VdbCursor c;
             c.reset();
             return c.query(s.lv[ev.grid_level], ev.ijk).occ;

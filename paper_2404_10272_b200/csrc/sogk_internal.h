@@ -81,6 +81,10 @@ struct VdbBuildArgs {
     uint32_t* total_leaves;  // [1]
 };
 cudaError_t launch_vdb_build(const VdbBuildArgs& a, cudaStream_t st);
+// build_distance (sogk_distance.cu): exact chessboard distances of a dense grid into dist
+// (int32 per voxel); scratch has the same size; *any_occupied = 0 means all_empty()
+cudaError_t launch_distance_build(const GridDev& dense, int32_t* dist, int32_t* scratch,
+                                  unsigned* any_occupied, cudaStream_t st);
 // to_dense (sparse.hpp:374-383): expands a VDB into a dense payload
 cudaError_t launch_vdb_to_dense(const GridDev& vdb, uint8_t* bits, int64_t nbytes,
                                 cudaStream_t st);

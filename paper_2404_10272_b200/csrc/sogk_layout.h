@@ -40,6 +40,7 @@ struct GridDev {
     const uint64_t* value_mask;
     const uint32_t* prefix;
     const uint64_t* leaves;
+    const int32_t* dist;   // DistanceGrid (distance.hpp:15-43): chessboard distance per voxel
 };
 
 struct SamplerDev {

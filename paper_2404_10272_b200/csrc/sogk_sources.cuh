@@ -59,7 +59,8 @@ struct RaysFromCamera {
 
 template <int AN, bool CASC>
 struct PickAn {
-    using Sub = typename std::conditional<AN == SOGK_HDDA, HddaAn, DdaAn>::type;
+    using Sub = typename std::conditional<
+        AN == SOGK_HDDA, HddaAn, typename std::conditional<AN == SOGK_CD, CdAn, DdaAn>::type>::type;
     using type = AnyAn<Sub, CASC>;
 };
 
@@ -82,7 +83,15 @@ struct PickAn {
             case 12: return L::template FN<1, true, false, 0>(__VA_ARGS__);                       \
             case 13: return L::template FN<1, true, false, 1>(__VA_ARGS__);                       \
             case 14: return L::template FN<1, true, true, 0>(__VA_ARGS__);                        \
-            default: return L::template FN<1, true, true, 1>(__VA_ARGS__);                        \
+            case 15: return L::template FN<1, true, true, 1>(__VA_ARGS__);                        \
+            case 16: return L::template FN<2, false, false, 0>(__VA_ARGS__);                      \
+            case 17: return L::template FN<2, false, false, 1>(__VA_ARGS__);                      \
+            case 18: return L::template FN<2, false, true, 0>(__VA_ARGS__);                       \
+            case 19: return L::template FN<2, false, true, 1>(__VA_ARGS__);                       \
+            case 20: return L::template FN<2, true, false, 0>(__VA_ARGS__);                       \
+            case 21: return L::template FN<2, true, false, 1>(__VA_ARGS__);                       \
+            case 22: return L::template FN<2, true, true, 0>(__VA_ARGS__);                        \
+            default: return L::template FN<2, true, true, 1>(__VA_ARGS__);                        \
         }                                                                                         \
     } while (0)
 

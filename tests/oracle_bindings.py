@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "libsog_oracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libsogref.so")
 
-DDA, HDDA = 0, 1
+DDA, HDDA, CD = 0, 1, 2
 BRANCH, SKIP = 0, 1
 CONSTANT, LINEAR = 0, 1
 SCENE_KINDS = {"blobs": 0, "shell": 1, "sponge": 2, "random": 3}
@@ -90,6 +90,10 @@ class Oracle:
         L.og_dense_create.argtypes = [_i32p, _dp, C.c_double, _u8p]
         L.og_sparse_build.restype = C.c_void_p
         L.og_sparse_build.argtypes = [C.c_void_p]
+        L.og_distance_build.restype = C.c_void_p
+        L.og_distance_build.argtypes = [C.c_void_p]
+        L.og_distance_data.restype = C.c_void_p
+        L.og_distance_data.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         L.og_grid_free.argtypes = [C.c_void_p]
         L.og_sparse_serialize.restype = C.c_int64
         L.og_sparse_serialize.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
@@ -154,6 +158,21 @@ class Oracle:
         self._owned.append(h)
         return h
 
+    def distance(self, g: Grid) -> int:
+        d = self.dense(g)
+        h = self.L.og_distance_build(d)
+        self._owned.append(h)
+        return h
+
+    def distance_field(self, g: Grid):
+        """build_distance (distance.hpp:45-103) -> (int32 [z][y][x], all_empty)."""
+        h = self.distance(g)
+        ae = C.c_int32(0)
+        p = self.L.og_distance_data(h, C.byref(ae))
+        n = int(g.res[0]) * int(g.res[1]) * int(g.res[2])
+        a = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_int32)), shape=(n,)).copy()
+        return a.reshape(g.res[2], g.res[1], g.res[0]), bool(ae.value)
+
     def sog1(self, g: Grid) -> bytes:
         s = self.sparse(g)
         n = self.L.og_sparse_serialize(s, None, 0)
@@ -176,7 +195,8 @@ class Oracle:
     def sampler(self, levels, analyzer, kernel, sched_kind, dt0, growth=0.0, cascade=False,
                 spin_cap=64) -> _OgSampler:
         s = _OgSampler()
-        handles = [self.sparse(g) if analyzer == HDDA else self.dense(g) for g in levels]
+        handles = [self.sparse(g) if analyzer == HDDA else self.distance(g) if analyzer == CD
+                   else self.dense(g) for g in levels]
         for i, h in enumerate(handles):
             s.levels[i] = h
         s.n_levels = len(handles)
@@ -247,6 +267,8 @@ class RefLib:
                                        _i64p, _dp, _dp, _u32p, _u8p, _i32p]
         L.ref_collect_events.restype = C.c_int64
         L.ref_collect_events.argtypes = [C.c_void_p, _dp, C.c_int64, _i32p, _dp, _i64p]
+        L.ref_build_distance.restype = C.c_int
+        L.ref_build_distance.argtypes = [_i32p, _dp, C.c_double, _u8p, _i32p]
         L.ref_scene_primitives.restype = C.c_int
         L.ref_scene_primitives.argtypes = [C.c_int, _i32p, _dp, C.c_double, C.c_uint64, C.c_double,
                                            C.c_int, _dp, C.c_int, _dp]
@@ -282,6 +304,13 @@ class RefLib:
                                  fraction, count, threshold, levels, bits, wm, vx)
         return [Grid(tuple(int(x) for x in r), tuple(wm[3 * b:3 * b + 3]), float(vx[b]),
                      bits[b * nb:(b + 1) * nb].copy()) for b in range(levels)]
+
+    def distance_field(self, g: Grid):
+        """the reference build_distance -> (int32 [z][y][x], all_empty)."""
+        out = np.zeros(int(g.res[0]) * int(g.res[1]) * int(g.res[2]), np.int32)
+        ae = self.L.ref_build_distance(np.asarray(g.res, np.int32), np.asarray(g.wmin, np.float64),
+                                       g.voxel, np.ascontiguousarray(g.bits, np.uint8), out)
+        return out.reshape(g.res[2], g.res[1], g.res[0]), bool(ae)
 
     def scene_primitives(self, kind, res=128, seed=1, fraction=0.05, count=12,
                          wmin=(-1.0, -1.0, -1.0), extent=2.0):

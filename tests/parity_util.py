@@ -4,9 +4,9 @@ from __future__ import annotations
 
 import numpy as np
 
-from oracle_bindings import BRANCH, CONSTANT, DDA, HDDA, LINEAR, SKIP, Grid, Packed  # noqa: F401
+from oracle_bindings import BRANCH, CD, CONSTANT, DDA, HDDA, LINEAR, SKIP, Grid, Packed  # noqa: F401
 
-VARIANTS = [(DDA, BRANCH), (DDA, SKIP), (HDDA, BRANCH), (HDDA, SKIP)]
+VARIANTS = [(DDA, BRANCH), (DDA, SKIP), (HDDA, BRANCH), (HDDA, SKIP), (CD, BRANCH), (CD, SKIP)]
 
 
 def host_grid(P, t, bits) -> Grid:
@@ -28,6 +28,8 @@ def gpu_grids(P, levels, analyzer):
     dense = [P.DenseGrid(transform_of(P, g), g.bits) for g in levels]
     if analyzer == HDDA:
         return [P.build_sparse(d) for d in dense]
+    if analyzer == CD:
+        return [P.build_distance(d) for d in dense]
     return dense
 
 
