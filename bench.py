@@ -228,8 +228,10 @@ def run_gpu(args):
     # --- grids: rank 0's payloads broadcast once over NVLink (NCCL), VDB built per rank (K1)
     grids = []
     build_ms = []
+    dist_ms = []
+    dist_grids = []
     for o in wl.objects:
-        dense_lv, vdb_lv = [], []
+        dense_lv, vdb_lv, cd_lv = [], [], []
         for t, bits in o["levels"]:
             d_bits = torch.from_numpy(bits).to(dev)
             broadcast_payload(d_bits)  # once, NCCL over NVLink; rank 0's payload wins
@@ -241,9 +243,16 @@ def run_gpu(args):
             e1.record()
             torch.cuda.synchronize()
             build_ms.append(e0.elapsed_time(e1))
+            e0.record()
+            cg = P.build_distance(dg)
+            e1.record()
+            torch.cuda.synchronize()
+            dist_ms.append(e0.elapsed_time(e1))
             dense_lv.append(dg)
             vdb_lv.append(vg)
+            cd_lv.append(cg)
         grids.append((dense_lv, vdb_lv))
+        dist_grids.append(cd_lv)
     vdb_bytes = [sum(int(v.memory_bytes()) for v in vl) for _, vl in grids]
     dense_bytes = [sum(int(t.payload_bytes()) for t, _ in o["levels"]) for o in wl.objects]
 
@@ -251,12 +260,14 @@ def run_gpu(args):
         "hdda_skip": (P.Analyzer.hdda, P.KernelKind.skip),
         "dda_branch": (P.Analyzer.dda, P.KernelKind.branch),
         "dda_skip": (P.Analyzer.dda, P.KernelKind.skip),
+        "cd_skip": (P.Analyzer.cd, P.KernelKind.skip),
     }
     if args.variants:
         variants = {k: v for k, v in variants.items() if k in args.variants.split(",")}
     samplers = {}
     for vname, (an, kk) in variants.items():
-        samplers[vname] = [P.Sampler(grids[i][1] if an == P.Analyzer.hdda else grids[i][0], an, kk,
+        samplers[vname] = [P.Sampler(grids[i][1] if an == P.Analyzer.hdda else
+                                     dist_grids[i] if an == P.Analyzer.cd else grids[i][0], an, kk,
                                      wl.schedule, cascade=wl.cascade) for i in range(n_obj)]
 
     nr = wl.rays_per_object()
@@ -518,6 +529,7 @@ def run_gpu(args):
                           "frac": step_gbs / peak,
                           "basis": "N_rays*(64+16) + N_samples*24 + VDB bytes (SURVEY §8d)"},
         "vdb_build_ms": build_ms,
+        "distance_build_ms": dist_ms,
         "grid_bytes": {"dense": dense_bytes, "vdb_sog1": vdb_bytes},
         "render": ({"what": "render_frame fused on the GPU (Camera::pixel_ray -> sampling -> "
                              "composite_detailed -> Image::set_pixel per pixel, no sample arrays), "

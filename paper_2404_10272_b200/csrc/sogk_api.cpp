@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -162,14 +163,47 @@ struct sogk_grid {
     }
 };
 
+// Pass-1 -> pass-2 workspaces, one per (device, stream): work on one stream is ordered, so
+// samplers can share it; a sampler's slabs stay valid until another count on that stream.
+struct Workspace {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    uint64_t gen = 0;
+};
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, void*>, Workspace>& ws_registry() {
+    static auto* m = new std::map<std::pair<int, void*>, Workspace>(); // never destroyed
+    return *m;
+}
+static Workspace* workspace_peek(void* stream) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = ws_registry().find({dev, stream});
+    return it == ws_registry().end() ? nullptr : &it->second;
+}
+static int workspace_for(void* stream, size_t need, Workspace** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace& w = ws_registry()[{dev, stream}];
+    if (w.bytes < need) {
+        cudaFree(w.ptr); // synchronous: work still reading it has finished
+        w.ptr = nullptr;
+        w.bytes = 0;
+        ++w.gen; // whatever it held is gone
+        CK(cudaMalloc(&w.ptr, need), "sampler workspace");
+        w.bytes = need;
+    }
+    *out = &w;
+    return SOGK_OK;
+}
+
 struct sogk_sampler {
     Variant v{};
     SamplerDev dev{};
     sogk_sampler_desc desc{};
     int n_levels = 0;
-    // count-pass scratch: tile states + dynamic tile counter
-    void* ws = nullptr;
-    size_t ws_bytes = 0;
     // sogk_sample_host scratch
     void* hb = nullptr;
     size_t hb_bytes = 0;
@@ -178,7 +212,6 @@ struct sogk_sampler {
     size_t rb_bytes = 0;
 
     ~sogk_sampler() {
-        cudaFree(ws);
         cudaFree(hb);
         cudaFree(rb);
     }
@@ -196,41 +229,49 @@ struct sogk_sampler {
     int64_t* render_stats() const { return static_cast<int64_t*>(rb); }
     int64_t* render_packed() const { return reinterpret_cast<int64_t*>(static_cast<char*>(rb) + 256); }
 
-    // pass 1 -> pass 2 handshake: the sample slabs of the last count call
+    // pass 1 -> pass 2 handshake: the sample slabs of the last count call live in the
+    // workspace of (device, stream); they are this sampler's as long as no other count ran
+    // there since (generation check) -- otherwise pass 2 takes the exact cold path
+    Workspace* wsp = nullptr;
+    uint64_t my_gen = 0;
     const void* last_rays = nullptr;
     int64_t last_first = -1, last_n = -1;
     bool last_cam = false;
     int64_t slab_cap = 256; // C: slab entries per ray (SOGK_SLAB; 0 = resume-only)
+    double slab_budget = 24.0 * (1ull << 30); // bytes of slabs per workspace (SOGK_SLAB_BUDGET_GB)
 
-    // workspace = [scan tile states | counters (64 B) | resume states | overflow list | slabs]
     int64_t cap_for(int64_t n) const {
-        // keep the slabs below ~24 GiB of HBM; a smaller slab only sends more rays to tail_kernel
+        // keep the slabs within the budget; a smaller slab only sends more rays to
+        // tail_kernel (exact either way)
         int64_t c = slab_cap;
-        while (c > 0 && double(n) * double(c) * 13.0 > 24.0 * (1ull << 30)) c -= 8;
+        while (c > 0 && double(n) * double(c) * 13.0 > slab_budget) c -= 4;
         return c < 0 ? 0 : c;
     }
     static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+    // workspace = [scan tile states | counters (64 B) | resume states | overflow list | slabs]
     size_t need_bytes(int64_t n) const {
         const size_t e = size_t(n) * size_t(cap_for(n));
         return scan_off(n) + al(resume_bytes(n)) + al(size_t(n) * 4) + al(e * 8) + al(e * 4) + al(e);
     }
-    int ensure_ws(int64_t n) {
-        const size_t need = need_bytes(n);
-        if (need <= ws_bytes) return SOGK_OK;
-        cudaFree(ws);
-        ws = nullptr;
-        ws_bytes = 0;
-        last_n = -1;
-        CK(cudaMalloc(&ws, need), "sampler workspace");
-        ws_bytes = need;
+    // binds the (device, stream) workspace, grown to fit n rays, and claims it for a count
+    int claim_ws(int64_t n, void* stream) {
+        Workspace* w = nullptr;
+        int st = workspace_for(stream, need_bytes(n), &w);
+        if (st) return st;
+        wsp = w;
+        my_gen = ++w->gen;
         return SOGK_OK;
     }
+    bool owns_ws(void* stream) const {
+        return wsp && wsp->gen == my_gen && wsp == workspace_peek(stream);
+    }
+    void* ws() const { return wsp->ptr; }
     static size_t scan_off(int64_t n) { return ((size_t(scan_tiles(n)) * 8 + 64 + 255) / 256) * 256; }
-    uint64_t* tiles() const { return static_cast<uint64_t*>(ws); }
+    uint64_t* tiles() const { return static_cast<uint64_t*>(ws()); }
     // counters: [scan tile counter (u32 in a u64 slot) | overflow counter]
     unsigned* ovf_ctr(int64_t n) const { return reinterpret_cast<unsigned*>(tiles() + scan_tiles(n) + 1); }
     SlabDev slab(int64_t n) const {
-        char* p = static_cast<char*>(ws) + scan_off(n);
+        char* p = static_cast<char*>(ws()) + scan_off(n);
         SlabDev S{};
         S.C = cap_for(n);
         const size_t e = size_t(n) * size_t(S.C);
@@ -867,6 +908,7 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     s->v.branch = desc->kernel == SOGK_BRANCH ? 1 : 0;
     s->v.linear = desc->schedule == SOGK_LINEAR ? 1 : 0;
     if (const char* e = std::getenv("SOGK_SLAB")) s->slab_cap = (std::max(0, std::atoi(e)) + 3) & ~3; // multiple of 4
+    if (const char* e = std::getenv("SOGK_SLAB_BUDGET_GB")) s->slab_budget = std::max(0.0, std::atof(e)) * double(1ull << 30);
     for (int b = 0; b < n_levels; ++b) s->dev.lv[b] = levels[b]->dev();
     s->dev.n_levels = n_levels;
     s->dev.spin_cap = desc->spin_cap > 0 ? desc->spin_cap : SOGK_DEFAULT_SPIN_CAP;
@@ -917,10 +959,10 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
         return fail(SOGK_INVALID_ARG, "NULL device buffer");
     CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
     if (n == 0) return SOGK_OK;
-    int st = s->ensure_ws(n);
+    int st = s->claim_ws(n, stream);
     if (st) return st;
     const int64_t tiles = scan_tiles(n);
-    CK(cudaMemsetAsync(s->ws, 0, size_t(tiles) * 8 + 64, S(stream)), "workspace reset");
+    CK(cudaMemsetAsync(s->ws(), 0, size_t(tiles) * 8 + 64, S(stream)), "workspace reset");
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
     const SlabDev slab = s->slab(n);
@@ -967,7 +1009,7 @@ static int write_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
     // the slabs are valid when pass 1 ran on this sampler with the same rays
-    const bool same = s->last_n == n && s->last_cam == (cam != nullptr) &&
+    const bool same = s->owns_ws(stream) && s->last_n == n && s->last_cam == (cam != nullptr) &&
                       (cam ? s->last_first == first : s->last_rays == d_rays);
     const SlabDev slab = same ? s->slab(n) : SlabDev{};
     CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed,
