@@ -237,21 +237,22 @@ struct sogk_sampler {
     const void* last_rays = nullptr;
     int64_t last_first = -1, last_n = -1;
     bool last_cam = false;
-    int64_t slab_cap = 256; // C: slab entries per ray (SOGK_SLAB; 0 = resume-only)
+    int64_t slab_cap = 128; // C: run records per ray (SOGK_SLAB; 0 = resume-only)
     double slab_budget = 24.0 * (1ull << 30); // bytes of slabs per workspace (SOGK_SLAB_BUDGET_GB)
 
     int64_t cap_for(int64_t n) const {
         // keep the slabs within the budget; a smaller slab only sends more rays to
         // tail_kernel (exact either way)
         int64_t c = slab_cap;
-        while (c > 0 && double(n) * double(c) * 13.0 > slab_budget) c -= 4;
+        while (c > 0 && double(n) * double(c) * 16.0 > slab_budget) c -= 4;
         return c < 0 ? 0 : c;
     }
     static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
-    // workspace = [scan tile states | counters (64 B) | resume states | overflow list | slabs]
+    // workspace = [scan tile states | counters (64 B) | resume states | overflow list |
+    //              run counts | run slabs]
     size_t need_bytes(int64_t n) const {
         const size_t e = size_t(n) * size_t(cap_for(n));
-        return scan_off(n) + al(resume_bytes(n)) + al(size_t(n) * 4) + al(e * 8) + al(e * 4) + al(e);
+        return scan_off(n) + al(resume_bytes(n)) + 2 * al(size_t(n) * 4) + e * sizeof(RunRec);
     }
     // binds the (device, stream) workspace, grown to fit n rays, and claims it for a count
     int claim_ws(int64_t n, void* stream) {
@@ -279,11 +280,10 @@ struct sogk_sampler {
         p += al(resume_bytes(n));
         S.ovf_list = reinterpret_cast<uint32_t*>(p);
         p += al(size_t(n) * 4);
-        S.t = reinterpret_cast<double*>(p);
-        p += al(e * 8);
-        S.cell = reinterpret_cast<uint32_t*>(p);
-        p += al(e * 4);
-        S.lvl = reinterpret_cast<uint8_t*>(p);
+        S.nruns = reinterpret_cast<int32_t*>(p);
+        p += al(size_t(n) * 4);
+        S.runs = reinterpret_cast<RunRec*>(p);
+        (void)e;
         S.ovf_ctr = ovf_ctr(n);
         return S;
     }
@@ -907,7 +907,7 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     s->v.cascade = cascade ? 1 : 0;
     s->v.branch = desc->kernel == SOGK_BRANCH ? 1 : 0;
     s->v.linear = desc->schedule == SOGK_LINEAR ? 1 : 0;
-    if (const char* e = std::getenv("SOGK_SLAB")) s->slab_cap = (std::max(0, std::atoi(e)) + 3) & ~3; // multiple of 4
+    if (const char* e = std::getenv("SOGK_SLAB")) s->slab_cap = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("SOGK_SLAB_BUDGET_GB")) s->slab_budget = std::max(0.0, std::atof(e)) * double(1ull << 30);
     for (int b = 0; b < n_levels; ++b) s->dev.lv[b] = levels[b]->dev();
     s->dev.n_levels = n_levels;

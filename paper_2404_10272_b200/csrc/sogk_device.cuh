@@ -382,11 +382,12 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
 #ifndef SOGK_HDDA_SMEM
 #define SOGK_HDDA_SMEM 1
 #endif
+// Kernels using the node analyzers or the cascade launch 1-D blocks of at most kGeomBlock
+// threads (per-thread shared-memory columns).
+constexpr int kGeomBlock = 128;
 #if SOGK_HDDA_SMEM
 // The per-ray geometry lives in shared memory (one column per thread, SoA: conflict-free),
-// which keeps ~22 registers out of the traversal loop and so raises occupancy; the loop is
-// latency-bound.  Kernels using HddaAn launch 1-D blocks of at most kGeomBlock threads.
-constexpr int kGeomBlock = 128;
+// which keeps ~22 registers out of the traversal loop.
 struct HddaGeomSmem {
     double e[3][kGeomBlock], dv[3][kGeomBlock], iv[3][kGeomBlock];
     double te[kGeomBlock], tx[kGeomBlock];

@@ -15,14 +15,22 @@ struct Variant {
     int linear;   // 1: linear schedule
 };
 
-// Pass 1 -> pass 2 state (sampler workspace): every ray's first samples in a fixed
-// per-ray slab of C entries (t, cell, level), the resume state of rays whose runs did not
-// all fit (Resume::tag bits 8.. = samples in the slab), and the list of those rays.
+// A sample run: the ladder points one occupied event contributes, S[start .. start + n)
+// of its ray (n = the next run's start, or the ray's slab fill for its last run).
+struct __align__(16) RunRec {
+    double first;  // first ladder point of the run
+    uint32_t cell; // x | y << 10 | z << 20 (pack_cell)
+    uint32_t sl;   // start (24 bits) | (Level | grid_level << 2) << 24
+};
+constexpr uint32_t kRunStartMax = (1u << 24) - 1;
+
+// Pass 1 -> pass 2 state (sampler workspace): every ray's first runs in a fixed per-ray slab
+// of C run records, the number of records per ray, the resume state of rays whose runs did
+// not all fit (Resume::tag bits 8.. = samples covered by the slab), and the list of those rays.
 struct SlabDev {
-    double* t;          // [n][C]
-    uint32_t* cell;     // [n][C]
-    uint8_t* lvl;       // [n][C]
-    int64_t C;          // slab entries per ray; 0 = no slab (every ray resumes in tail_kernel)
+    RunRec* runs;       // [n][C]
+    int32_t* nruns;     // [n]
+    int64_t C;          // run records per ray; 0 = no slab (every ray resumes in tail_kernel)
     Resume* resume;     // [n]
     uint32_t* ovf_list; // [n]
     unsigned* ovf_ctr;  // [1], zeroed before pass 1

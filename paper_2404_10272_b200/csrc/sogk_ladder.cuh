@@ -132,6 +132,61 @@ SOGK_HD int64_t ladder_seek(double& t, double T, double dt0, double inv_dt0, dou
     }
 }
 
+// t after exactly k steps of  t <- t + dt  (constant step, t >= 0): the same binade argument
+// as seek_const -- once two consecutive in-binade steps are taken explicitly every further
+// in-binade step adds the same bit increment -- used to jump inside a binade.  A ladder that
+// cannot advance (t + dt == t) stays where it is.
+SOGK_HD double advance_const(double t, int64_t k, double dt, double inv_dt) {
+#pragma unroll 1
+    while (k > 0) {
+        if (k < 3) {
+            t = t + dt;
+            --k;
+            continue;
+        }
+        const double t0 = t;
+        const double t1 = t0 + dt;
+        const double t2 = t1 + dt;
+        k -= 2;
+        t = t2;
+        const int64_t b0 = dbits(t0), b1 = dbits(t1), b2 = dbits(t2);
+        const int64_t e0 = b0 >> 52;
+        if (e0 != (b2 >> 52) || e0 == 0) continue; // binade crossing or subnormal: keep stepping
+        const int64_t inc = b2 - b1;
+        if (inc <= 0) return t; // t + dt == t
+        const int64_t end = (e0 + 1) << 52;
+        const int64_t kmax = fix_quotient(end - 1 - b2, inc, (dfrom(end) - t2) * inv_dt);
+        const int64_t j = kmax < k ? kmax : k;
+        if (j <= 0) continue;
+        t = dfrom(b2 + j * inc);
+        k -= j;
+    }
+    return t;
+}
+
+// t after exactly k ladder steps t <- t + step(t) (StepSchedule::step, sampling.hpp:36-38);
+// the linear schedule is the constant step dt0 for points <= t_switch and is stepped
+// explicitly beyond
+template <int Sched>
+SOGK_HD double ladder_advance(double t, int64_t k, double dt0, double inv_dt0, double growth,
+                              double t_switch) {
+    if constexpr (Sched == 0) {
+        return advance_const(t, k, dt0, inv_dt0);
+    } else {
+#pragma unroll 1
+        while (k > 0 && t <= t_switch) { // constant regime, stepped (bounded by t_switch)
+            t = t + dt0;
+            --k;
+        }
+#pragma unroll 1
+        for (; k > 0; --k) {
+            const double g = growth * t;
+            t = t + ((dt0 < g) ? g : dt0);
+        }
+        return t;
+    }
+}
+
 template <int Sched>
 SOGK_HD double ladder_step(double t, double dt0, double growth) {
     if constexpr (Sched == 0) {

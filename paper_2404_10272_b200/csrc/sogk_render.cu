@@ -142,7 +142,24 @@ __global__ void __launch_bounds__(kRenderBlock)
     comp.store(r, result, rgb8);
 }
 
-// composite from the slabs of pass 1 (rays whose samples all fit: count <= C)
+// composite from the run slabs of pass 1 (rays whose runs all fit)
+template <int SCH>
+__device__ __forceinline__ long long composite_runs(Compositor<SCH>& comp, const SceneDev& sc,
+                                                    const Ray& ray, const SamplerDev& s,
+                                                    const RunRec* row, int nr, long long fill) {
+    for (int j = 0; j < nr; ++j) {
+        const RunRec a = row[j];
+        const long long start = a.sl & kRunStartMax;
+        const long long end = j + 1 < nr ? (long long)(row[j + 1].sl & kRunStartMax) : fill;
+        double t = a.first;
+        for (long long k = start; k < end; ++k) {
+            comp.add(sc, ray, s, t);
+            t = t + ladder_step<SCH>(t, s.dt0, s.growth);
+        }
+    }
+    return fill;
+}
+
 template <int SCH, class Src>
 __global__ void __launch_bounds__(kRenderBlock)
     composite_slab_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const Src src,
@@ -151,18 +168,18 @@ __global__ void __launch_bounds__(kRenderBlock)
     const int64_t r = (int64_t)blockIdx.x * kRenderBlock + threadIdx.x;
     if (r >= n) return;
     const long long cnt = __ldg(reinterpret_cast<const longlong2*>(packed) + r).y;
-    if (cnt > S.C) return; // render_tail_kernel
+    const int raw = cnt > 0 ? __ldg(S.nruns + r) : 0;
+    if (raw < 0) return; // overflowed: render_tail_kernel
     const Ray ray = src.load(r);
     Compositor<SCH> comp;
     comp.init();
-    const double* row = S.t + r * S.C;
-    for (long long k = 0; k < cnt; ++k) comp.add(sc, ray, s, __ldg(row + k));
+    composite_runs<SCH>(comp, sc, ray, s, S.runs + r * S.C, raw, cnt);
     comp.finish(sc, ray, s);
     comp.store(r, result, rgb8);
 }
 
-// rays whose samples overflowed the slab: the slab part, then the traversal resumed at
-// the first event that did not fit, all composited in order
+// rays whose runs overflowed the slab: the slab part, then the traversal resumed at the
+// first event that did not fit, all composited in order
 template <int AN, bool CASC, bool BR, int SCH, class Src>
 __global__ void __launch_bounds__(kRenderBlock)
     render_tail_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const Src src,
@@ -178,12 +195,11 @@ __global__ void __launch_bounds__(kRenderBlock)
         const Ray ray = src.load(r);
         Compositor<SCH> comp;
         comp.init();
-        const double* row = S.t + r * S.C;
-        for (long long k = 0; k < fill; ++k) comp.add(sc, ray, s, row[k]);
+        long long done = composite_runs<SCH>(comp, sc, ray, s, S.runs + r * S.C,
+                                             S.nruns[r] & 0x7fffffff, fill);
         RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
         gen.init(ray, s);
         gen.resume(s, res);
-        long long done = fill;
         Run run;
         while (done < total) {
             const int st = gen.step(s, run);
@@ -200,17 +216,6 @@ __global__ void __launch_bounds__(kRenderBlock)
     }
 }
 
-cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
-                             const double* rays, int64_t n, const int64_t* packed, const double* ts,
-                             double* result, uint8_t* rgb8, cudaStream_t st) {
-    const unsigned blocks = (unsigned)((n + kRenderBlock - 1) / kRenderBlock);
-    if (v.linear)
-        composite_kernel<1><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, n, packed, ts, result, rgb8);
-    else
-        composite_kernel<0><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, n, packed, ts, result, rgb8);
-    return cudaGetLastError();
-}
-
 struct RenderLaunch {
     template <int AN, bool CASC, bool BR, int SCH>
     static cudaError_t tail(const SamplerDev& s, const SceneDev& sc, const RaysFromCamera& src,
@@ -221,6 +226,17 @@ struct RenderLaunch {
         return cudaGetLastError();
     }
 };
+
+cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
+                             const double* rays, int64_t n, const int64_t* packed, const double* ts,
+                             double* result, uint8_t* rgb8, cudaStream_t st) {
+    const unsigned blocks = (unsigned)((n + kRenderBlock - 1) / kRenderBlock);
+    if (v.linear)
+        composite_kernel<1><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, n, packed, ts, result, rgb8);
+    else
+        composite_kernel<0><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, n, packed, ts, result, rgb8);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_render_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
                                     const CameraDev& cam, int64_t first, int64_t n,

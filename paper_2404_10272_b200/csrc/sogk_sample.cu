@@ -24,6 +24,9 @@ namespace sogk {
 
 constexpr int kBlock = 128;
 constexpr int kWriteBlock = 128;
+#ifndef SOGK_GATHER_SHORT
+#define SOGK_GATHER_SHORT 8
+#endif
 #ifndef SOGK_CASC_MINB
 #define SOGK_CASC_MINB 1 // the same for the cascade variants
 #endif
@@ -167,92 +170,61 @@ __device__ __forceinline__ void count_invalid(long long r, int64_t* packed, uint
 // ---------------------------------------------------------------------------
 // pass 1: per-ray counts, status, counters, slab samples, resume state
 // ---------------------------------------------------------------------------
-// Pass-1 slab staging: a lane puts its samples in a 4-slot shared-memory group (SoA,
-// conflict-free) and writes each group of 4 slab entries as one 256-bit (t) and one 128-bit
-// (cell) store; slab rows are 32-byte aligned (C is a multiple of 4).
-__device__ __forceinline__ void stage_flush(const SlabDev& S, int64_t idx, const double* st,
-                                            const uint32_t* sc) {
-    static_cast<double4*>(__builtin_assume_aligned(S.t + idx, 32))[0] =
-        make_double4(st[0], st[kBlock], st[2 * kBlock], st[3 * kBlock]);
-    static_cast<uint4*>(__builtin_assume_aligned(S.cell + idx, 16))[0] =
-        make_uint4(sc[0], sc[kBlock], sc[2 * kBlock], sc[3 * kBlock]);
-}
-
 template <int AN, bool CASC, bool BR, int SCH, class Src>
 __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MINB)
     count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
                  int32_t* __restrict__ counters, const SlabDev S) {
-    __shared__ double stage_t[4 * kBlock];
-    __shared__ uint32_t stage_c[4 * kBlock];
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     Stats5 acc;
     if (r < n) {
         const Ray ray = src.load(r);
         if (!ray_valid(ray)) {
             count_invalid(r, packed, status, counters, acc);
+            if (S.nruns) S.nruns[r] = 0;
         } else {
             RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
             gen.init(ray, s);
-            const int64_t row = r * S.C;
+            RunRec* const row = S.runs + r * S.C;
             long long c = 0;
-            int filled = 0;     // samples in the slab
-            bool ovf = false;   // slab full: the rest of the ray comes from its resume state
-            bool stored = false;
-            bool tail_flushed = false; // the group holding the slab's last sample is written
-            double* const st_t = stage_t + threadIdx.x;
-            uint32_t* const st_c = stage_c + threadIdx.x;
+            int nr = 0;       // run records in the slab
+            long long filled = 0; // samples they cover
+            bool ovf = false; // slab full: the rest of the ray comes from its resume state
             for (;;) { // one flat loop: one analyzer step per iteration
                 Event ev;
                 double t_last0;
                 const int st = gen.step_event(s, ev, t_last0);
                 if (st == 0) break;
                 if (st == 1) continue;
-                int k = 0; // points of this event
-                if (!ovf) { // the reference loop itself: while (t <= t1) { push(t); t += step(t); }
-                    // single grids: the 2-bit Level rides in the cell word's spare top bits
-                    // (cells pack 3 x 10 bits); cascades also need grid_level, in S.lvl
-                    const uint32_t cw = CASC ? pack_cell(ev.ijk)
-                                             : pack_cell(ev.ijk) | ((uint32_t)ev.level << 30);
-                    const uint8_t lvl = (uint8_t)(ev.level | (ev.grid_level << 2));
-                    double t = gen.t_last;
-                    const int room = (int)S.C - filled;
-                    while (t <= ev.t1 && k < room) {
-                        const int p = filled + k;
-                        st_t[(p & 3) * kBlock] = t;
-                        st_c[(p & 3) * kBlock] = cw;
-                        if (CASC) S.lvl[row + p] = lvl;
-                        if ((p & 3) == 3) stage_flush(S, row + p - 3, st_t, st_c);
-                        t = t + ladder_step<SCH>(t, s.dt0, s.growth);
-                        ++k;
-                    }
-                    gen.t_last = t;
-                    if (t <= ev.t1) { // slab full inside this event: it restarts in tail_kernel
-                        ovf = true;
-                        // this event's samples may have recycled the staging slots of the
-                        // group holding position filled - 1; that group was written whole first
-                        tail_flushed = filled + k >= (filled & ~3) + 4;
-                        Run run;
-                        run.ijk[0] = ev.ijk[0];
-                        run.ijk[1] = ev.ijk[1];
-                        run.ijk[2] = ev.ijk[2];
-                        run.tag = gen.an.resume_tag();
-                        run.t0 = ev.t0;
-                        run.t_last0 = t_last0;
-                        store_resume(S.resume + r, run, filled);
-                        stored = true;
-                    } else {
-                        filled += k;
-                    }
-                }
-                if (ovf) k += gen.seek_to(s, ev.t1); // counted, not stored
+                const double first = gen.t_last;
+                // the event's ladder points (t0, t1], counted in closed form
+                const int k = gen.seek_to(s, ev.t1);
                 if (BR) gen.kernel_lookups += k;
                 c += k;
+                if (k == 0 || ovf) continue;
+                if (nr < S.C && filled + k <= (long long)kRunStartMax) {
+                    RunRec rec;
+                    rec.first = first;
+                    rec.cell = pack_cell(ev.ijk);
+                    rec.sl = (uint32_t)filled | ((uint32_t)(ev.level | (ev.grid_level << 2)) << 24);
+                    row[nr++] = rec; // one 128-bit store per run
+                    filled += k;
+                } else { // the run that does not fit restarts in tail_kernel
+                    ovf = true;
+                    Run run;
+                    run.ijk[0] = ev.ijk[0];
+                    run.ijk[1] = ev.ijk[1];
+                    run.ijk[2] = ev.ijk[2];
+                    run.tag = gen.an.resume_tag();
+                    run.t0 = ev.t0;
+                    run.t_last0 = t_last0;
+                    store_resume(S.resume + r, run, (int)filled);
+                }
             }
-            // the partial last group (a slab row is private to its ray: written whole)
-            if ((filled & 3) && !tail_flushed) stage_flush(S, row + (filled & ~3), st_t, st_c);
+            // run count; bit 31 marks a ray whose runs overflowed the slab
+            if (S.nruns) S.nruns[r] = gen.undefined() ? 0 : (nr | (ovf ? (int)0x80000000 : 0));
             count_finish(gen, r, c, packed, status, counters, acc);
-            if (stored && c > 0 && !gen.undefined()) {
+            if (ovf && c > 0 && !gen.undefined()) {
                 S.ovf_list[atomicAdd(S.ovf_ctr, 1u)] = (uint32_t)r;
                 ++acc.ovf;
             }
@@ -464,77 +436,145 @@ __global__ void __launch_bounds__(kWriteBlock)
     w.flush(o, s);
 }
 
-// pass 2: slabs -> packed arrays.  A block owns kGather consecutive rays, whose samples
-// form one contiguous output range; thread i handles output samples i, i + kGather, ...
-// (consecutive threads on consecutive samples: every store is coalesced and every output
-// sector is written whole by one warp).  The owning ray of a sample is a binary search
-// over the block's offsets in shared memory.  Samples past a ray's slab are tail_kernel's.
+// pass 2: run slabs -> packed arrays.  A block owns kGather consecutive rays: their samples
+// form one contiguous output range and their runs one local run index space (block scan of
+// the per-ray run counts in shared memory).  Thread i expands runs i, i + kGather, ...: it
+// finds the owning ray by a branch-free binary search over the block's run offsets, reads
+// the run record (and the next one's start for its length) and writes the run's samples
+// with the reference recurrence t <- t + step(t).  Consecutive threads take consecutive
+// runs, whose samples are adjacent in the output.  Samples past a ray's slab are
+// tail_kernel's.
 constexpr int kGather = 256;
 
-template <int SCH, bool CASC>
+template <int SCH>
 __global__ void __launch_bounds__(kGather)
     gather_kernel(const __grid_constant__ SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
                   const SlabDev S, int64_t ray_index_base, const Out o) {
-    __shared__ long long s_base[2];
-    __shared__ int s_off[kGather]; // ray offsets relative to the block's first sample
-    __shared__ int s_fill[kGather];
-    const int tid = threadIdx.x;
+    __shared__ int s_roff[kGather + 1]; // local run offsets (exclusive), INT_MAX past the rays
+    __shared__ long long s_off[kGather]; // output offset of each ray
+    __shared__ int s_fill[kGather];      // samples of each ray covered by its slab
+    __shared__ int s_nr[kGather];
+    __shared__ int s_wsum[kGather / 32];
+    constexpr int kShort = SOGK_GATHER_SHORT; // runs up to this long: expanded by their own lane
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t r0 = (int64_t)blockIdx.x * kGather;
-    const int nr = (int)(n - r0 < kGather ? n - r0 : kGather);
+    const int nrays = (int)(n - r0 < kGather ? n - r0 : kGather);
     const int64_t r = r0 + tid;
-    longlong2 pi = make_longlong2(0, 0);
-    if (tid < nr) pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
-    if (tid == 0) s_base[0] = pi.x;
-    if (tid == nr - 1) s_base[1] = pi.x + pi.y;
-    __syncthreads();
-    const long long O0 = s_base[0], O1 = s_base[1];
-    // a block's samples (<= kGather * max per-ray count) fit 31 bits
-    s_off[tid] = tid < nr ? (int)(pi.x - O0) : INT_MAX;
-    int fill = (int)(pi.y < S.C ? pi.y : S.C);
-    if (tid < nr && pi.y > S.C) fill = S.resume[r].tag >> 8; // overflowed: what pass 1 put in the slab
-    s_fill[tid] = fill;
-    __syncthreads();
-    const int m = (int)(O1 - O0);
-    // kUnroll independent samples per thread and iteration (stride kGather: stores stay
-    // coalesced), so each thread keeps several slab loads in flight
-    constexpr int kUnroll = 4;
-    for (int e0 = tid; e0 < m; e0 += kUnroll * kGather) {
-        int j[kUnroll], k[kUnroll];
-        bool ok[kUnroll];
+    int nr = 0;
+    if (tid < nrays) {
+        const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
+        const int raw = pi.y > 0 ? __ldg(S.nruns + r) : 0;
+        nr = raw & 0x7fffffff;
+        s_off[tid] = pi.x;
+        // every sample of the ray is in its runs, unless they overflowed the slab: then the
+        // slab covers the samples before the resume point (Resume::tag >> 8)
+        s_fill[tid] = raw < 0 ? (S.resume[r].tag >> 8) : (int)pi.y;
+    }
+    s_nr[tid] = nr;
+    // block exclusive scan of the run counts
+    int v = nr;
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const int e = e0 + u * kGather;
-            int jj = 0; // largest jj with s_off[jj] <= e: branch-free binary search
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += y;
+    }
+    if (lane == 31) s_wsum[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < kGather / 32 ? s_wsum[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, d);
+            if (lane >= d) w += y;
+        }
+        if (lane < kGather / 32) s_wsum[lane] = w;
+    }
+    __syncthreads();
+    const int incl = v + (wid > 0 ? s_wsum[wid - 1] : 0);
+    s_roff[tid] = tid < nrays ? incl - nr : INT_MAX;
+    const int total = s_wsum[kGather / 32 - 1];
+    __syncthreads();
+    for (int base = 0; base < total; base += kGather) { // block-uniform trip count
+        const int q = base + tid;
+        const bool have = q < total;
+        double first = 0.0;
+        long long g0 = 0;
+        int n = 0;
+        uint32_t cell = 0;
+        uint8_t lv = 0;
+        int32_t ri = 0;
+        if (have) {
+            int j = 0; // largest j with s_roff[j] <= q: branch-free binary search
 #pragma unroll
             for (int step = kGather / 2; step > 0; step >>= 1)
-                jj += (s_off[jj + step] <= e) ? step : 0;
-            j[u] = jj;
-            k[u] = e - s_off[jj];
-            ok[u] = e < m && k[u] < s_fill[jj];
+                j += (s_roff[j + step] <= q) ? step : 0;
+            const int local = q - s_roff[j];
+            const RunRec* rec = S.runs + (r0 + j) * S.C + local;
+            const RunRec a = *rec;
+            const int start = (int)(a.sl & kRunStartMax);
+            const int end = local + 1 < s_nr[j] ? (int)(rec[1].sl & kRunStartMax) : s_fill[j];
+            first = a.first;
+            g0 = s_off[j] + start;
+            n = end - start;
+            cell = a.cell;
+            lv = (uint8_t)(a.sl >> 24);
+            ri = (int32_t)(ray_index_base + r0 + j);
         }
-        double t[kUnroll];
-        uint32_t cw[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            t[u] = 0.0;
-            cw[u] = 0;
-            if (ok[u]) {
-                const int64_t i = (r0 + j[u]) * S.C + k[u];
-                t[u] = __ldcs(S.t + i);
-                cw[u] = __ldcs(reinterpret_cast<const unsigned int*>(S.cell) + i);
+        if (n <= kShort) { // the common case: a voxel's few points, by its own lane
+            double t = first;
+            for (int k = 0; k < n; ++k) {
+                const double tn = t + ladder_step<SCH>(t, s.dt0, s.growth);
+                const long long g = g0 + k;
+                __stcs(o.t_starts + g, t);
+                if (o.t_ends) __stcs(o.t_ends + g, tn);
+                if (o.ray_indices) __stcs(o.ray_indices + g, ri);
+                if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, cell);
+                if (o.levels) o.levels[g] = lv;
+                t = tn;
             }
         }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            if (!ok[u]) continue;
-            const long long g = O0 + e0 + u * kGather;
-            __stcs(o.t_starts + g, t[u]);
-            if (o.t_ends) __stcs(o.t_ends + g, t[u] + ladder_step<SCH>(t[u], s.dt0, s.growth));
-            if (o.ray_indices) __stcs(o.ray_indices + g, (int32_t)(ray_index_base + r0 + j[u]));
-            if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, CASC ? cw[u] : cw[u] & 0x3fffffffu);
-            if (o.levels) {
-                const int64_t i = (r0 + j[u]) * S.C + k[u];
-                o.levels[g] = CASC ? S.lvl[i] : (uint8_t)(cw[u] >> 30);
+        // long runs (tiles): the whole warp writes each one, point k from the run's first
+        // point by the closed-form ladder advance (exact), consecutive lanes on consecutive
+        // points
+        unsigned lm = __ballot_sync(0xffffffffu, n > kShort);
+        while (lm) {
+            const int src = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const double f = __shfl_sync(0xffffffffu, first, src);
+            const long long gb = __shfl_sync(0xffffffffu, g0, src);
+            const int nn = __shfl_sync(0xffffffffu, n, src);
+            const uint32_t ce = __shfl_sync(0xffffffffu, cell, src);
+            const int lvl = __shfl_sync(0xffffffffu, (int)lv, src);
+            const int32_t rr = __shfl_sync(0xffffffffu, ri, src);
+            // constant schedule: after two explicit in-binade steps every further in-binade
+            // step adds the same bit increment (sogk_ladder.cuh), so point k >= 2 is
+            // bits(t2) + (k - 2) * inc while it stays in t0's binade
+            double t1 = 0.0;
+            int64_t b2 = 0, inc = 0, kfast = 1;
+            if (SCH == 0) {
+                t1 = f + s.dt0;
+                const double t2 = t1 + s.dt0;
+                const int64_t b0 = dbits(f), b1 = dbits(t1);
+                b2 = dbits(t2);
+                inc = b2 - b1;
+                const int64_t e0 = b0 >> 52;
+                if (e0 == (b2 >> 52) && e0 != 0 && inc > 0) {
+                    const int64_t end = (e0 + 1) << 52;
+                    kfast = 2 + fix_quotient(end - 1 - b2, inc, (dfrom(end) - t2) * s.inv_dt0);
+                }
+            }
+            for (int k = lane; k < nn; k += 32) {
+                double t;
+                if (SCH == 0 && k <= kfast)
+                    t = k == 0 ? f : (k == 1 ? t1 : dfrom(b2 + (int64_t)(k - 2) * inc));
+                else
+                    t = ladder_advance<SCH>(f, k, s.dt0, s.inv_dt0, s.growth, s.t_switch);
+                const long long g = gb + k;
+                __stcs(o.t_starts + g, t);
+                if (o.t_ends) __stcs(o.t_ends + g, t + ladder_step<SCH>(t, s.dt0, s.growth));
+                if (o.ray_indices) __stcs(o.ray_indices + g, rr);
+                if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, ce);
+                if (o.levels) o.levels[g] = (uint8_t)lvl;
             }
         }
     }
@@ -631,7 +671,7 @@ struct Launch {
             return cudaGetLastError();
         }
         const unsigned gb = (unsigned)((n + kGather - 1) / kGather);
-        gather_kernel<SCH, CASC><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
+        gather_kernel<SCH><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
         const unsigned tg = tail_grid(n);
         if (vec)
             tail_kernel<AN, CASC, BR, SCH, true, Src><<<tg, kWriteBlock, 0, st>>>(s, src, packed, *S, base, o);

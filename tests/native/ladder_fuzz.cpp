@@ -54,6 +54,21 @@ int main(int argc, char** argv) {
             nb = (long)sogk::ladder_seek<1>(b, T, dt0, 1.0 / dt0, g, t_switch(dt0, g), stalled);
         }
         jumps += nb > 6;
+        // ladder_advance: k steps from t0 == the recurrence k times
+        {
+            const long k = (long)(rng() % 64 == 0 ? rng() % 5000 : rng() % 80);
+            double c = t0;
+            for (long j = 0; j < k; ++j) c += sched == 0 ? dt0 : ((dt0 < g * c) ? g * c : dt0);
+            const double d = sched == 0
+                                 ? sogk::ladder_advance<0>(t0, k, dt0, 1.0 / dt0, g, DBL_MAX)
+                                 : sogk::ladder_advance<1>(t0, k, dt0, 1.0 / dt0, g, t_switch(dt0, g));
+            if (sogk::dbits(c) != sogk::dbits(d)) {
+                if (bad < 10)
+                    std::printf("ADVANCE MISMATCH sched=%d dt0=%.17g t0=%.17g k=%ld: %.17g vs %.17g\n",
+                                sched, dt0, t0, k, c, d);
+                ++bad;
+            }
+        }
         if (na != nb || sogk::dbits(a) != sogk::dbits(b) || stalled) {
             if (bad < 10)
                 std::printf("MISMATCH sched=%d dt0=%.17g g=%.17g t0=%.17g T=%.17g: naive %ld %.17g seek %ld %.17g\n",
