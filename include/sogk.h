@@ -252,6 +252,10 @@ int sogk_composite(const sogk_sampler* s, const sogk_scene* scene, const double*
 int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_camera* cam,
                        int64_t first_pixel, int64_t n, double* d_result, uint8_t* d_rgb8,
                        int64_t* d_stats, void* stream);
+/* The whole frame into HOST buffers: h_rgb8[height][width][3] (Image bytes, rows top to
+ * bottom) and h_stats[SOGK_STATS_LEN]; synchronous. */
+int sogk_render_frame_host(sogk_sampler* s, const sogk_scene* scene, const sogk_camera* cam,
+                           uint8_t* h_rgb8, int64_t* h_stats, void* stream);
 
 /* ---- host input generators (deterministic; no GPU needed) ---------------
  * Restatements of the reference generators so that identical inputs can be

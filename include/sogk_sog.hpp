@@ -23,7 +23,10 @@
 #include <string>
 #include <vector>
 
+#include "sog/camera.hpp"
+#include "sog/distance.hpp"
 #include "sog/io.hpp"
+#include "sog/render.hpp"
 #include "sog/sampling.hpp"
 #include "sogk.h"
 
@@ -125,6 +128,32 @@ inline DeviceSparseGrid build_sparse(const DenseGrid& d, void* stream = nullptr)
     return build_sparse(DeviceDenseGrid(d, stream), stream);
 }
 
+/// DistanceGrid (distance.hpp:15-43) in HBM: the grid the CD analyzer marches.
+class DeviceDistanceGrid {
+public:
+    DeviceDistanceGrid(sogk_grid* g, const GridTransform& t) : t_(t), h_(g, GridDeleter{}) {}
+    const GridTransform& transform() const { return t_; }
+    sogk_grid* handle() const { return h_.get(); }
+    /// the reference DistanceGrid (same values: both transforms are exact)
+    DistanceGrid to_host() const {
+        std::vector<std::int32_t> d(std::size_t(t_.voxel_count()));
+        std::int32_t ae = 0;
+        check(sogk_grid_download_distance(h_.get(), d.data(), d.size(), &ae));
+        return DistanceGrid(t_, std::move(d), ae != 0);
+    }
+
+private:
+    GridTransform t_;
+    GridHandle h_;
+};
+
+/// build_distance (distance.hpp:45-103) on the GPU.
+inline DeviceDistanceGrid build_distance(const DeviceDenseGrid& d, void* stream = nullptr) {
+    sogk_grid* g = nullptr;
+    check(sogk_grid_build_distance(d.handle(), stream, &g));
+    return DeviceDistanceGrid(g, d.transform());
+}
+
 /// Packed sample intervals of a ray batch (sogk.h output contract).
 struct PackedSamples {
     std::vector<std::int64_t> packed_info; // [n][2] offset, count
@@ -157,14 +186,19 @@ struct SamplerDeleter {
     void operator()(sogk_sampler* s) const { sogk_sampler_destroy(s); }
 };
 
-/// One variant of the reference's variant matrix (bench.hpp:30-64): dense+dda+{branch,skip}
-/// or sparse+hdda+{branch,skip}, over one grid or a cascade (sampling.hpp:222-462).
+/// One variant of the reference's variant matrix (bench.hpp:30-64): dense+dda, sparse+hdda or
+/// dense+cd (the distance grid), each {branch, skip}, over one grid or a cascade
+/// (sampling.hpp:222-462).
 class Sampler {
 public:
     Sampler(const DeviceDenseGrid& g, KernelKind k, const StepSchedule& s)
         : Sampler({g.handle()}, SOGK_DDA, k, s, false) {}
     Sampler(const DeviceSparseGrid& g, KernelKind k, const StepSchedule& s)
         : Sampler({g.handle()}, SOGK_HDDA, k, s, false) {}
+    Sampler(const DeviceDistanceGrid& g, KernelKind k, const StepSchedule& s)
+        : Sampler({g.handle()}, SOGK_CD, k, s, false) {}
+    Sampler(const std::vector<DeviceDistanceGrid>& cascade, KernelKind k, const StepSchedule& s)
+        : Sampler(handles(cascade), SOGK_CD, k, s, true) {}
     Sampler(const std::vector<DeviceDenseGrid>& cascade, KernelKind k, const StepSchedule& s)
         : Sampler(handles(cascade), SOGK_DDA, k, s, true) {}
     Sampler(const std::vector<DeviceSparseGrid>& cascade, KernelKind k, const StepSchedule& s)
@@ -253,6 +287,69 @@ inline SampleRun run_sampler(const Ray& ray, const DeviceSparseGrid& g, KernelKi
 /// reference's render_frame / run_matrix consume.
 inline std::function<SampleRun(const Ray&)> make_sampler(const Sampler& s) {
     return [s](const Ray& r) { return s(r); };
+}
+
+/// AnalyticScene (render.hpp:58-92) in HBM.
+class DeviceScene {
+public:
+    explicit DeviceScene(const AnalyticScene& scene) {
+        scene.validate();
+        std::vector<sogk_primitive> p;
+        for (const Primitive& q : scene.primitives) {
+            sogk_primitive c{};
+            c.shape = q.shape == Primitive::Shape::sphere ? SOGK_SPHERE : SOGK_BOX;
+            for (int a = 0; a < 3; ++a) {
+                c.center[a] = q.center[a];
+                c.lo[a] = q.lo[a];
+                c.hi[a] = q.hi[a];
+                c.color[a] = q.color[a];
+            }
+            c.radius = q.radius;
+            c.density = q.density;
+            p.push_back(c);
+        }
+        const double bg[3] = {scene.background.x, scene.background.y, scene.background.z};
+        sogk_scene* h = nullptr;
+        check(sogk_scene_create(p.data(), std::int32_t(p.size()), bg, &h));
+        h_.reset(h, [](sogk_scene* x) { sogk_scene_destroy(x); });
+    }
+    sogk_scene* handle() const { return h_.get(); }
+
+private:
+    std::shared_ptr<sogk_scene> h_;
+};
+
+/// render_frame (bench.hpp:424-461) on the GPU: every pixel sampled and composited
+/// (composite_detailed, render.hpp:97-118) in two kernels, the image and the FrameResult
+/// counters back on the host.  Pixels agree with the reference within one 8-bit level
+/// (CUDA exp vs glibc exp); the counters are exact.
+struct GpuFrame {
+    Image image;
+    long lookups = 0, steps = 0, samples = 0;
+};
+inline GpuFrame render_frame(const Sampler& s, const DeviceScene& scene, const Camera& cam,
+                             void* stream = nullptr) {
+    sogk_camera c{};
+    const double pos[3] = {cam.position.x, cam.position.y, cam.position.z};
+    const double tgt[3] = {cam.target.x, cam.target.y, cam.target.z};
+    const double up[3] = {cam.up.x, cam.up.y, cam.up.z};
+    check(sogk_camera_setup(pos, tgt, up, cam.vfov_deg, cam.width, cam.height, cam.t_far, &c));
+    const std::int64_t n = std::int64_t(cam.width) * cam.height;
+    std::vector<std::uint8_t> rgb(std::size_t(n) * 3);
+    std::int64_t stats[SOGK_STATS_LEN] = {};
+    check(sogk_render_frame_host(s.handle(), scene.handle(), &c, rgb.data(), stats, stream));
+    GpuFrame f;
+    f.image = Image(cam.width, cam.height);
+    for (int y = 0; y < cam.height; ++y)
+        for (int x = 0; x < cam.width; ++x) {
+            const std::size_t i = (std::size_t(y) * cam.width + x) * 3;
+            // Image::set_pixel of the 8-bit value reproduces the byte exactly
+            f.image.set_pixel(x, y, Vec3{rgb[i] / 255.0, rgb[i + 1] / 255.0, rgb[i + 2] / 255.0});
+        }
+    f.lookups = long(stats[SOGK_STAT_ANALYZER_LOOKUPS] + stats[SOGK_STAT_KERNEL_LOOKUPS]);
+    f.steps = long(stats[SOGK_STAT_ANALYZER_STEPS]);
+    f.samples = long(stats[SOGK_STAT_TOTAL_SAMPLES]);
+    return f;
 }
 
 } // namespace sog::gpu

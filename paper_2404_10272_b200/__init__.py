@@ -129,6 +129,7 @@ _SIGS = {
     "sogk_scene_destroy": (C.c_int, [_vp]),
     "sogk_composite": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sogk_render_camera": (C.c_int, [_vp, _vp, C.POINTER(_Camera), _i64, _i64, _vp, _vp, _vp, _vp]),
+    "sogk_render_frame_host": (C.c_int, [_vp, _vp, C.POINTER(_Camera), _vp, _vp, _vp]),
     "sogk_scene_generate": (C.c_int, [C.c_int, C.POINTER(_Transform), _u64, _dbl, _i32, _dbl, _vp, C.POINTER(_dbl)]),
     "sogk_scene_cascade": (C.c_int, [C.c_int, C.POINTER(_Transform), _u64, _dbl, _i32, _dbl, _i32, _vp, C.POINTER(_Transform)]),
     "sogk_probe_rays": (C.c_int, [C.POINTER(_Transform), _i64, _u64, _vp]),

@@ -1184,6 +1184,29 @@ int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_came
     return SOGK_OK;
 }
 
+int sogk_render_frame_host(sogk_sampler* s, const sogk_scene* scene, const sogk_camera* cam,
+                           uint8_t* h_rgb8, int64_t* h_stats, void* stream) {
+    if (!s || !scene || !cam || !h_rgb8) return fail(SOGK_INVALID_ARG, "NULL argument");
+    const int64_t n = int64_t(cam->width) * cam->height;
+    uint8_t* d_rgb = nullptr;
+    int64_t* d_stats = nullptr;
+    cudaError_t e = dalloc(&d_rgb, size_t(n) * 3);
+    if (e == cudaSuccess) e = dalloc(&d_stats, SOGK_STATS_LEN);
+    int st = e == cudaSuccess ? SOGK_OK : cuda_fail(e, "render buffers");
+    if (st == SOGK_OK)
+        st = sogk_render_camera(s, scene, cam, 0, n, nullptr, d_rgb, d_stats, stream);
+    if (st == SOGK_OK) {
+        e = cudaMemcpyAsync(h_rgb8, d_rgb, size_t(n) * 3, cudaMemcpyDeviceToHost, S(stream));
+        if (e == cudaSuccess && h_stats)
+            e = cudaMemcpyAsync(h_stats, d_stats, SOGK_STATS_LEN * 8, cudaMemcpyDeviceToHost, S(stream));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+        if (e != cudaSuccess) st = cuda_fail(e, "render D2H");
+    }
+    cudaFree(d_rgb);
+    cudaFree(d_stats);
+    return st;
+}
+
 int sogk_camera_rays(const sogk_camera* cam, int64_t first_pixel, int64_t n, double* d_rays,
                      void* stream) {
     if (!camera_range_ok(cam, first_pixel, n) || (n && !d_rays))

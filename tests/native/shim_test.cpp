@@ -79,6 +79,44 @@ int main() {
     for (std::size_t r = 0; r < rays.size(); ++r)
         cm += oc.samples(r) != run_cascade_sampler(rays[r], sc, KernelKind::skip, lin).samples;
     EXPECT(cm == 0, "%ld cascade ray mismatches", cm);
+    // CD analyzer (run_sampler(ray, dense, dist, ...), sampling.hpp:198-212) and build_distance
+    const DistanceGrid dist = build_distance(dense);
+    const gpu::DeviceDistanceGrid ddist = gpu::build_distance(ddense);
+    {
+        const DistanceGrid back = ddist.to_host();
+        long dm = 0;
+        for (int z = 0; z < 64; ++z)
+            for (int y = 0; y < 64; ++y)
+                for (int x = 0; x < 64; ++x) dm += back.at({x, y, z}) != dist.at({x, y, z});
+        EXPECT(dm == 0 && back.all_empty() == dist.all_empty(), "%ld distance values differ", dm);
+        for (KernelKind k : {KernelKind::branch, KernelKind::skip}) {
+            const gpu::PackedSamples o = gpu::Sampler(ddist, k, scheds[0]).sample_rays(rays);
+            long m = 0;
+            for (std::size_t r = 0; r < rays.size(); ++r) {
+                const SampleRun a = run_sampler(rays[r], dense, dist, k, scheds[0]);
+                const SampleRun b = o.run(r);
+                m += a.samples != b.samples || a.analyzer_lookups != b.analyzer_lookups ||
+                     a.analyzer_steps != b.analyzer_steps || a.kernel_lookups != b.kernel_lookups;
+            }
+            EXPECT(m == 0, "%ld CD ray mismatches (kernel %d)", m, int(k));
+        }
+    }
+    // render_frame (bench.hpp:424-461): the reference's image vs the GPU frame
+    {
+        BenchAssets assets;
+        assets.scene = gen.scene;
+        assets.dense.levels.push_back(dense);
+        assets.camera = cam;
+        assets.schedule = scheds[0];
+        const FrameResult ref = render_frame(assets, [&](const Ray& r) {
+            return run_sampler(r, sparse, KernelKind::skip, scheds[0]);
+        }, 1);
+        const gpu::GpuFrame g = gpu::render_frame(gpu::Sampler(dvdb, KernelKind::skip, scheds[0]),
+                                                  gpu::DeviceScene(gen.scene), cam);
+        EXPECT(psnr(g.image, ref.image) >= 40.0, "render PSNR %.1f dB", psnr(g.image, ref.image));
+        EXPECT(g.lookups == ref.lookups && g.steps == ref.steps && g.samples == ref.samples,
+               "frame counters differ");
+    }
     // errors like the reference
     bool threw = false;
     try {
@@ -87,7 +125,7 @@ int main() {
         threw = true;
     }
     EXPECT(threw, "negative step did not throw std::invalid_argument");
-    std::printf("%s: %zu rays x 4 variants x 2 schedules + cascade, %d failures\n",
+    std::printf("%s: %zu rays x 4 variants x 2 schedules + cascade + CD + render, %d failures\n",
                 failures ? "FAILED" : "OK", rays.size(), failures);
     return failures ? 1 : 0;
 }
