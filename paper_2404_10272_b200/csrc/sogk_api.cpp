@@ -89,6 +89,7 @@ struct sogk_grid {
     uint64_t* value_mask = nullptr;
     uint32_t* prefix = nullptr;
     uint64_t* leaves = nullptr;
+    int32_t* table = nullptr;
     uint32_t* region_leaves = nullptr;
     uint32_t* total_leaves = nullptr;
     uint64_t leaf_capacity = 0;
@@ -110,6 +111,7 @@ struct sogk_grid {
         cudaFree(child_mask);
         cudaFree(value_mask);
         cudaFree(prefix);
+        cudaFree(table);
         cudaFree(leaves);
         cudaFree(region_leaves);
         cudaFree(total_leaves);
@@ -143,6 +145,7 @@ struct sogk_grid {
         g.value_mask = value_mask;
         g.prefix = prefix;
         g.leaves = leaves;
+        g.table = table;
         g.dist = dist;
         return g;
     }
@@ -377,6 +380,7 @@ static cudaError_t alloc_vdb(sogk_grid* g) {
     if ((e = dalloc(&g->child_mask, g->nreg * 64)) != cudaSuccess) return e;
     if ((e = dalloc(&g->value_mask, g->nreg * 64)) != cudaSuccess) return e;
     if ((e = dalloc(&g->prefix, g->nreg * 64)) != cudaSuccess) return e;
+    if ((e = dalloc(&g->table, g->nreg * 4096)) != cudaSuccess) return e;
     if ((e = dalloc(&g->region_leaves, g->nreg)) != cudaSuccess) return e;
     if ((e = dalloc(&g->total_leaves, 1)) != cudaSuccess) return e;
     return cudaSuccess;
@@ -406,6 +410,7 @@ int sogk_grid_build_vdb(const sogk_grid* d, void* stream, sogk_grid** out) {
     a.child_mask = g->child_mask;
     a.value_mask = g->value_mask;
     a.prefix = g->prefix;
+    a.table = g->table;
     a.leaves = g->leaves;
     a.region_leaves = g->region_leaves;
     a.total_leaves = g->total_leaves;
@@ -496,7 +501,7 @@ int sogk_grid_get_info(const sogk_grid* g, sogk_grid_info* out) {
     // memory_bytes(SparseGrid) == SOG1 size (io.hpp:227-238)
     out->memory_bytes = (4 + 4 + 12 + 24 + 8 + 4) + entries * 13 + internal * 4096 +
                         g->leaf_count * 64;
-    out->device_bytes = g->nreg * (4 + 64 * (8 + 8 + 4) + 4) + 4 + int64_t(g->leaf_capacity) * 64;
+    out->device_bytes = g->nreg * (4 + 64 * (8 + 8 + 4) + 4 + 4096 * 4) + 4 + int64_t(g->leaf_capacity) * 64;
     return SOGK_OK;
 }
 
@@ -821,7 +826,17 @@ int sogk_grid_load_sog1(const uint8_t* bytes, size_t len, void* stream, sogk_gri
     if (e == cudaSuccess && !leaves.empty())
         e = cudaMemcpy(g->leaves, leaves.data(), leaves.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->total_leaves, &tl, 4, cudaMemcpyHostToDevice);
-    (void)stream;
+    if (e == cudaSuccess) {
+        VdbBuildArgs a{};
+        for (int k = 0; k < 3; ++k) a.R[k] = g->R[k];
+        a.root = g->root;
+        a.child_mask = g->child_mask;
+        a.value_mask = g->value_mask;
+        a.prefix = g->prefix;
+        a.table = g->table;
+        e = launch_vdb_table(a, S(stream));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+    }
     if (e != cudaSuccess) {
         delete g;
         return cuda_fail(e, "SOG1 upload");

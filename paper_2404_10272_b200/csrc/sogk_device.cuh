@@ -199,38 +199,32 @@ struct VdbCursor {
         Query q;
         const unsigned lx = (unsigned)(ijk[0] - lo[0]), ly = (unsigned)(ijk[1] - lo[1]),
                        lz = (unsigned)(ijk[2] - lo[2]);
-        if ((lx | ly | lz) < 8u) { // cached leaf hit (Accessor fast path, sparse.hpp:229-233)
-            const uint64_t w = __ldg(g.leaves + leaf * 8 + lz);
-            q.occ = (w >> ((ly << 3) | lx)) & 1ull;
-            q.level = LV_VOXEL;
-            q.ext = 1;
-            return q;
+        if ((lx | ly | lz) >= 8u) { // not the cached leaf (Accessor fast path, sparse.hpp:229-233)
+            q.occ = false;
+            q.level = LV_ROOT_TILE;
+            q.ext = 128;
+            if (!in_bounds(g, ijk)) return q; // background root tile at region_origin (:164-165)
+            const int region = ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7);
+            const int32_t node = __ldg(g.root + region);
+            q.level = LV_INTERNAL_TILE;
+            if (node < 0) { // collapsed region (root tile)
+                q.occ = node == kRootOccupied;
+                return q;
+            }
+            const int ci = ((((ijk[2] >> 3) & 15) * 16 + ((ijk[1] >> 3) & 15)) * 16) + ((ijk[0] >> 3) & 15);
+            const int32_t code = __ldg(g.table + (int64_t)node * 4096 + ci); // child table
+            if (code < 0) { // tile child (:205-208)
+                q.occ = code == kTileOccupied;
+                q.level = LV_LEAF_TILE;
+                q.ext = 8;
+                return q;
+            }
+            leaf = code;
+            lo[0] = ijk[0] & ~7;
+            lo[1] = ijk[1] & ~7;
+            lo[2] = ijk[2] & ~7;
         }
-        q.occ = false;
-        q.level = LV_ROOT_TILE;
-        q.ext = 128;
-        if (!in_bounds(g, ijk)) return q; // background root tile at region_origin (:164-165)
-        const int region = ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7);
-        const int32_t node = __ldg(g.root + region);
-        q.level = LV_INTERNAL_TILE;
-        if (node < 0) { // collapsed region (root tile)
-            q.occ = node == kRootOccupied;
-            return q;
-        }
-        const int ci = ((((ijk[2] >> 3) & 15) * 16 + ((ijk[1] >> 3) & 15)) * 16) + ((ijk[0] >> 3) & 15);
-        const int64_t wi = (int64_t)node * 64 + (ci >> 6);
-        const uint64_t cm = __ldg(g.child_mask + wi);
-        const int b = ci & 63;
-        if (!((cm >> b) & 1ull)) { // tile child (:205-208)
-            q.occ = (__ldg(g.value_mask + wi) >> b) & 1ull;
-            q.level = LV_LEAF_TILE;
-            q.ext = 8;
-            return q;
-        }
-        leaf = (int64_t)__ldg(g.prefix + wi) + __popcll(cm & ((1ull << b) - 1ull));
-        lo[0] = ijk[0] & ~7;
-        lo[1] = ijk[1] & ~7;
-        lo[2] = ijk[2] & ~7;
+        // the leaf word of ijk (cached leaf or just found)
         const uint64_t w = __ldg(g.leaves + leaf * 8 + (ijk[2] & 7));
         q.occ = (w >> (((ijk[1] & 7) << 3) | (ijk[0] & 7))) & 1ull;
         q.level = LV_VOXEL;

@@ -87,8 +87,11 @@ struct VdbBuildArgs {
     uint64_t* leaves;    // [nreg*4096*8] worst case
     uint32_t* region_leaves; // [nreg] scratch
     uint32_t* total_leaves;  // [1]
+    int32_t* table;          // [nreg*4096] child table (sogk_layout.h)
 };
 cudaError_t launch_vdb_build(const VdbBuildArgs& a, cudaStream_t st);
+// the child table of a VDB whose root/masks/prefix are set (built or loaded)
+cudaError_t launch_vdb_table(const VdbBuildArgs& a, cudaStream_t st);
 // build_distance (sogk_distance.cu): exact chessboard distances of a dense grid into dist
 // (int32 per voxel); scratch has the same size; *any_occupied = 0 means all_empty()
 cudaError_t launch_distance_build(const GridDev& dense, int32_t* dist, int32_t* scratch,

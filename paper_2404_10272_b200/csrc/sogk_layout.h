@@ -13,6 +13,9 @@
 //                           (leaf index = prefix[w] + popc(child_mask[w] & below(ci)))
 //   leaves[leaf][8]         u64: word z holds leaf bytes (z*8 + y), bit x — byte-identical
 //                           to LeafNode::bytes_ (sparse.hpp:21-25)
+//   table[node][4096]       i32: child ci's leaf index, or kTileEmpty / kTileOccupied — the
+//                           masks + prefix flattened into one lookup for traversal (the
+//                           reference's InternalNode kinds_/slots_, sparse.hpp:101-106)
 // Leaves are stored in (region, ci) order, which is also SOG1 order.
 #pragma once
 #include <cstdint>
@@ -23,6 +26,8 @@ namespace sogk {
 
 constexpr int32_t kRootEmpty = -1;
 constexpr int32_t kRootOccupied = -2;
+constexpr int32_t kTileEmpty = -1;
+constexpr int32_t kTileOccupied = -2;
 constexpr int SOGK_CONSTANT_SCHED = 0;
 constexpr int SOGK_LINEAR_SCHED = 1;
 
@@ -40,6 +45,7 @@ struct GridDev {
     const uint64_t* value_mask;
     const uint32_t* prefix;
     const uint64_t* leaves;
+    const int32_t* table;
     const int32_t* dist;   // DistanceGrid (distance.hpp:15-43): chessboard distance per voxel
 };
 

@@ -156,13 +156,39 @@ __global__ void __launch_bounds__(kBuildThreads) vdb_fill_kernel(const VdbBuildA
     }
 }
 
+// child table: one CTA per node, every child's leaf index (prefix + popcount, as K1 placed
+// the leaves) or its tile value
+__global__ void __launch_bounds__(kBuildThreads) vdb_table_kernel(const VdbBuildArgs a) {
+    const int r = blockIdx.x;
+    if (a.root[r] < 0) return; // collapsed regions have no node
+    const uint64_t* cm = a.child_mask + (int64_t)r * 64;
+    const uint64_t* vm = a.value_mask + (int64_t)r * 64;
+    const uint32_t* pf = a.prefix + (int64_t)r * 64;
+    for (int ci = threadIdx.x; ci < 4096; ci += kBuildThreads) {
+        const uint64_t m = cm[ci >> 6];
+        const int b = ci & 63;
+        int32_t v;
+        if ((m >> b) & 1ull) v = (int32_t)(pf[ci >> 6] + __popcll(m & ((1ull << b) - 1ull)));
+        else v = ((vm[ci >> 6] >> b) & 1ull) ? kTileOccupied : kTileEmpty;
+        a.table[(int64_t)r * 4096 + ci] = v;
+    }
+}
+
+cudaError_t launch_vdb_table(const VdbBuildArgs& a, cudaStream_t st) {
+    const int nreg = a.R[0] * a.R[1] * a.R[2];
+    vdb_table_kernel<<<nreg, kBuildThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_vdb_build(const VdbBuildArgs& a, cudaStream_t st) {
     const int nreg = a.R[0] * a.R[1] * a.R[2];
     vdb_classify_kernel<<<nreg, kBuildThreads, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     vdb_fill_kernel<<<nreg, kBuildThreads, 0, st>>>(a, nreg);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_vdb_table(a, st);
 }
 
 // to_dense (sparse.hpp:374-383): one thread per payload byte (8 consecutive voxels)
