@@ -402,33 +402,46 @@ def run_gpu(args):
                      ray_indices=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy(),
                      cells=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
                      stats=np.zeros(8, np.int64))
+        h_out["counters"] = torch.empty((nr, 3), dtype=torch.int32, pin_memory=True).numpy()
         lib = P.lib
 
-        def e2e_step(s):
+        def e2e_step(s, full):
+            # full: the packed intervals (t_starts, t_ends, ray_indices, cells); otherwise what
+            # the reference's run_sampler returns per ray (sampling.hpp:157-164): its sample
+            # buffer (packed t_starts + packed_info) and its three counters
             for o in range(n_obj):
                 rc = lib.sogk_sample_host(smp[o]._h, h_rays[s][o].data_ptr(), nr, 0, hcap,
                                           h_out["packed_info"].ctypes.data, h_out["t_starts"].ctypes.data,
-                                          h_out["t_ends"].ctypes.data, h_out["ray_indices"].ctypes.data,
-                                          h_out["cells"].ctypes.data, None, None, None,
+                                          h_out["t_ends"].ctypes.data if full else None,
+                                          h_out["ray_indices"].ctypes.data if full else None,
+                                          h_out["cells"].ctypes.data if full else None, None, None,
+                                          None if full else h_out["counters"].ctypes.data,
                                           h_out["stats"].ctypes.data, stream.cuda_stream or None)
                 P._check(rc, "sample_host")
 
-        for s in range(args.warmup):
-            e2e_step(s)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ts = time.perf_counter()
-        for k in range(args.steps):
-            e2e_step(args.warmup + k)
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - ts
-        if world > 1:
-            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        def timed(full):
+            for s in range(args.warmup):
+                e2e_step(s, full)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ts = time.perf_counter()
+            for k in range(args.steps):
+                e2e_step(args.warmup + k, full)
+            torch.cuda.synchronize()
+            sec = time.perf_counter() - ts
+            if world > 1:
+                tt = torch.tensor([sec], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                sec = float(tt.item())
+            return sec
+
+        e2e_s = timed(False)
+        e2e_full_s = timed(True)
         samples0 = sum(totals[(vname0, args.warmup + k, o)] for k in range(args.steps) for o in range(n_obj))
-        e2e = dict(seconds=e2e_s, h2d=nr * 64 * n_obj, d2h_per_run=samples0 * 24 / args.steps + nr * 16 * n_obj)
+        e2e = dict(seconds=e2e_s, h2d=nr * 64 * n_obj,
+                   d2h_per_run=samples0 * 8 / args.steps + nr * (16 + 12) * n_obj,
+                   full_seconds=e2e_full_s, full_d2h=samples0 * 24 / args.steps + nr * 16 * n_obj)
 
     # --- max over ranks
     def rmax(x):
@@ -541,7 +554,12 @@ def run_gpu(args):
     if e2e:
         line["e2e"] = {"value": total_rays / e2e["seconds"], "unit": "rays/s",
                        "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["d2h_per_run"]),
-                       "api": "sogk_sample_host (pinned host rays in, packed host samples out)"}
+                       "api": "sogk_sample_host: pinned host rays in; out, what run_sampler returns per ray "
+                              "(sampling.hpp:157-164): its samples (packed t_starts + packed_info) and "
+                              "its three counters",
+                       "full_intervals": {"value": total_rays / e2e["full_seconds"], "unit": "rays/s",
+                                          "d2h_bytes_per_step": int(e2e["full_d2h"]),
+                                          "outputs": "packed_info, t_starts, t_ends, ray_indices, cells"}}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(P, wl, args)
     print(json.dumps(line), flush=True)

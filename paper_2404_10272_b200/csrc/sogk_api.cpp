@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <cfloat>
 #include <cmath>
@@ -171,8 +172,13 @@ struct sogk_grid {
 struct Workspace {
     void* ptr = nullptr;
     size_t bytes = 0;
-    uint64_t gen = 0;
+    // the count whose slabs it holds: sampler id and the rays it ran on
+    uint64_t owner = 0;
+    const void* rays = nullptr;
+    int64_t first = -1, n = -1;
+    bool cam = false;
 };
+static std::atomic<uint64_t> g_sampler_ids{0};
 static std::mutex g_ws_mu;
 static std::map<std::pair<int, void*>, Workspace>& ws_registry() {
     static auto* m = new std::map<std::pair<int, void*>, Workspace>(); // never destroyed
@@ -194,7 +200,7 @@ static int workspace_for(void* stream, size_t need, Workspace** out) {
         cudaFree(w.ptr); // synchronous: work still reading it has finished
         w.ptr = nullptr;
         w.bytes = 0;
-        ++w.gen; // whatever it held is gone
+        w.owner = 0; // whatever it held is gone
         CK(cudaMalloc(&w.ptr, need), "sampler workspace");
         w.bytes = need;
     }
@@ -207,9 +213,13 @@ struct sogk_sampler {
     SamplerDev dev{};
     sogk_sampler_desc desc{};
     int n_levels = 0;
-    // sogk_sample_host scratch
+    // sogk_sample_host scratch, pipeline streams and pinned per-chunk stats
     void* hb = nullptr;
     size_t hb_bytes = 0;
+    bool lanes_ready = false;
+    cudaStream_t lanes[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
+    int64_t* h_chunk_stats = nullptr;
     // sogk_render_camera scratch: stats (256 B) | packed counts [n][2]
     void* rb = nullptr;
     size_t rb_bytes = 0;
@@ -217,6 +227,13 @@ struct sogk_sampler {
     ~sogk_sampler() {
         cudaFree(hb);
         cudaFree(rb);
+        if (lanes_ready) {
+            for (int l = 0; l < 3; ++l) {
+                cudaStreamDestroy(lanes[l]);
+                cudaEventDestroy(lane_ev[l]);
+            }
+            cudaFreeHost(h_chunk_stats);
+        }
     }
     int ensure_render(int64_t n) {
         const size_t need = size_t(n) * 16 + 256;
@@ -232,14 +249,10 @@ struct sogk_sampler {
     int64_t* render_stats() const { return static_cast<int64_t*>(rb); }
     int64_t* render_packed() const { return reinterpret_cast<int64_t*>(static_cast<char*>(rb) + 256); }
 
-    // pass 1 -> pass 2 handshake: the sample slabs of the last count call live in the
-    // workspace of (device, stream); they are this sampler's as long as no other count ran
-    // there since (generation check) -- otherwise pass 2 takes the exact cold path
-    Workspace* wsp = nullptr;
-    uint64_t my_gen = 0;
-    const void* last_rays = nullptr;
-    int64_t last_first = -1, last_n = -1;
-    bool last_cam = false;
+    // pass 1 -> pass 2 handshake: the run slabs of a count live in the workspace of the
+    // (device, stream) it ran on, tagged with the sampler and the rays; a write on that stream
+    // by the same sampler on the same rays uses them, anything else takes the exact cold path
+    const uint64_t id = ++g_sampler_ids;
     int64_t slab_cap = 128; // C: run records per ray (SOGK_SLAB; 0 = resume-only)
     double slab_budget = 24.0 * (1ull << 30); // bytes of slabs per workspace (SOGK_SLAB_BUDGET_GB)
 
@@ -257,25 +270,34 @@ struct sogk_sampler {
         const size_t e = size_t(n) * size_t(cap_for(n));
         return scan_off(n) + al(resume_bytes(n)) + 2 * al(size_t(n) * 4) + e * sizeof(RunRec);
     }
-    // binds the (device, stream) workspace, grown to fit n rays, and claims it for a count
-    int claim_ws(int64_t n, void* stream) {
+    // the (device, stream) workspace, grown to fit n rays and tagged for this count
+    int claim_ws(int64_t n, void* stream, const void* rays, bool cam, int64_t first, Workspace** out) {
         Workspace* w = nullptr;
         int st = workspace_for(stream, need_bytes(n), &w);
         if (st) return st;
-        wsp = w;
-        my_gen = ++w->gen;
+        w->owner = id;
+        w->rays = rays;
+        w->cam = cam;
+        w->first = first;
+        w->n = n;
+        *out = w;
         return SOGK_OK;
     }
-    bool owns_ws(void* stream) const {
-        return wsp && wsp->gen == my_gen && wsp == workspace_peek(stream);
+    // the workspace holding this sampler's slabs for these rays, or nullptr
+    Workspace* owned_ws(void* stream, const void* rays, bool cam, int64_t first, int64_t n) const {
+        Workspace* w = workspace_peek(stream);
+        if (!w || w->owner != id || w->n != n || w->cam != cam) return nullptr;
+        if (cam ? w->first != first : w->rays != rays) return nullptr;
+        return w;
     }
-    void* ws() const { return wsp->ptr; }
     static size_t scan_off(int64_t n) { return ((size_t(scan_tiles(n)) * 8 + 64 + 255) / 256) * 256; }
-    uint64_t* tiles() const { return static_cast<uint64_t*>(ws()); }
+    static uint64_t* tiles(const Workspace* w) { return static_cast<uint64_t*>(w->ptr); }
     // counters: [scan tile counter (u32 in a u64 slot) | overflow counter]
-    unsigned* ovf_ctr(int64_t n) const { return reinterpret_cast<unsigned*>(tiles() + scan_tiles(n) + 1); }
-    SlabDev slab(int64_t n) const {
-        char* p = static_cast<char*>(ws()) + scan_off(n);
+    static unsigned* ovf_ctr(const Workspace* w, int64_t n) {
+        return reinterpret_cast<unsigned*>(tiles(w) + scan_tiles(n) + 1);
+    }
+    SlabDev slab(const Workspace* w, int64_t n) const {
+        char* p = static_cast<char*>(w->ptr) + scan_off(n);
         SlabDev S{};
         S.C = cap_for(n);
         const size_t e = size_t(n) * size_t(S.C);
@@ -287,7 +309,7 @@ struct sogk_sampler {
         p += al(size_t(n) * 4);
         S.runs = reinterpret_cast<RunRec*>(p);
         (void)e;
-        S.ovf_ctr = ovf_ctr(n);
+        S.ovf_ctr = ovf_ctr(w, n);
         return S;
     }
 };
@@ -974,24 +996,21 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
         return fail(SOGK_INVALID_ARG, "NULL device buffer");
     CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
     if (n == 0) return SOGK_OK;
-    int st = s->claim_ws(n, stream);
+    Workspace* w = nullptr;
+    int st = s->claim_ws(n, stream, cam ? nullptr : d_rays, cam != nullptr, first, &w);
     if (st) return st;
     const int64_t tiles = scan_tiles(n);
-    CK(cudaMemsetAsync(s->ws(), 0, size_t(tiles) * 8 + 64, S(stream)), "workspace reset");
+    CK(cudaMemsetAsync(w->ptr, 0, size_t(tiles) * 8 + 64, S(stream)), "workspace reset");
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
-    const SlabDev slab = s->slab(n);
+    const SlabDev slab = s->slab(w, n);
     CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
                     d_status, d_counters, slab, S(stream)),
        "count launch");
     if (scan)
-        CK(launch_scan(n, d_packed, d_stats, s->tiles(),
-                       reinterpret_cast<unsigned int*>(s->tiles() + tiles), S(stream)),
+        CK(launch_scan(n, d_packed, d_stats, sogk_sampler::tiles(w),
+                       reinterpret_cast<unsigned int*>(sogk_sampler::tiles(w) + tiles), S(stream)),
            "scan launch");
-    s->last_rays = cam ? nullptr : d_rays;
-    s->last_cam = cam != nullptr;
-    s->last_first = first;
-    s->last_n = n;
     return SOGK_OK;
 }
 
@@ -1023,10 +1042,10 @@ static int write_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     if (!d_packed || !ts || (!cam && !d_rays)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
-    // the slabs are valid when pass 1 ran on this sampler with the same rays
-    const bool same = s->owns_ws(stream) && s->last_n == n && s->last_cam == (cam != nullptr) &&
-                      (cam ? s->last_first == first : s->last_rays == d_rays);
-    const SlabDev slab = same ? s->slab(n) : SlabDev{};
+    // the slabs are valid when pass 1 ran on this sampler, stream and rays
+    const Workspace* w = s->owned_ws(stream, cam ? nullptr : d_rays, cam != nullptr, first, n);
+    const bool same = w != nullptr;
+    const SlabDev slab = same ? s->slab(w, n) : SlabDev{};
     CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed,
                     same ? &slab : nullptr, base, ts, te, ri, ce, lv, S(stream)),
        "write launch");
@@ -1194,7 +1213,9 @@ int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_came
     if (st) return st;
     if (n == 0) return SOGK_OK;
     CK(launch_render_composite(s->v, s->dev, scene->dev, to_dev(*cam), first_pixel, n,
-                               s->render_packed(), s->slab(n), d_result, d_rgb8, S(stream)),
+                               s->render_packed(),
+                               s->slab(s->owned_ws(stream, nullptr, true, first_pixel, n), n), d_result,
+                               d_rgb8, S(stream)),
        "render launch");
     return SOGK_OK;
 }
@@ -1238,10 +1259,15 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     if (!s || !h_stats) return fail(SOGK_INVALID_ARG, "NULL argument");
     if (n < 0 || capacity < 0) return fail(SOGK_INVALID_ARG, "negative size");
     if (n > 0 && (!h_rays || !h_packed_info)) return fail(SOGK_INVALID_ARG, "NULL host buffer");
-    cudaStream_t st = S(stream);
-    // one scratch allocation: rays | packed | stats | status | counters | outputs
+    // Chunked pipeline over kLanes internal streams: chunk c's upload and pass 1 overlap the
+    // pass 2 and download of chunk c-1 (each stream has its own pass-1 -> pass-2 workspace).
+    // Offsets are made global on the device before download; the call is synchronous.
+    constexpr int kLanes = 3;
+    const int64_t chunk = std::max<int64_t>(65536, (n + 7) / 8);
+    const int64_t nchunks = n > 0 ? (n + chunk - 1) / chunk : 0;
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const size_t b_rays = al(size_t(n) * 64), b_packed = al(size_t(n) * 16), b_stats = al(64),
+    const size_t b_rays = al(size_t(n) * 64), b_packed = al(size_t(n) * 16),
+                 b_stats = al(size_t(std::max<int64_t>(nchunks, 1)) * SOGK_STATS_LEN * 8),
                  b_status = al(size_t(n)), b_ctr = al(size_t(n) * 12);
     const size_t b_ts = al(size_t(capacity) * 8), b_te = al(size_t(capacity) * 8),
                  b_ri = al(size_t(capacity) * 4), b_ce = al(size_t(capacity) * 4),
@@ -1253,6 +1279,14 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         s->hb_bytes = 0;
         CK(cudaMalloc(&s->hb, need), "host-path scratch");
         s->hb_bytes = need;
+    }
+    if (!s->lanes_ready) {
+        for (int l = 0; l < kLanes; ++l) {
+            CK(cudaStreamCreateWithFlags(&s->lanes[l], cudaStreamNonBlocking), "stream");
+            CK(cudaEventCreateWithFlags(&s->lane_ev[l], cudaEventDisableTiming), "event");
+        }
+        CK(cudaMallocHost(&s->h_chunk_stats, 64 * SOGK_STATS_LEN * 8), "pinned stats");
+        s->lanes_ready = true;
     }
     char* p = static_cast<char*>(s->hb);
     double* d_rays = reinterpret_cast<double*>(p);
@@ -1275,32 +1309,76 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     p += b_ce;
     uint8_t* d_lv = reinterpret_cast<uint8_t*>(p);
 
-    if (n > 0) CK(cudaMemcpyAsync(d_rays, h_rays, size_t(n) * 64, cudaMemcpyHostToDevice, st), "rays H2D");
-    int rc = sogk_sample_count(s, d_rays, n, d_packed, d_stats, h_status ? d_status : nullptr,
-                               h_counters ? d_ctr : nullptr, stream);
+    // order after the caller's prior work on `stream`
+    cudaEvent_t start_ev = s->lane_ev[0];
+    CK(cudaEventRecord(start_ev, S(stream)), "event");
+    for (int l = 0; l < kLanes; ++l) CK(cudaStreamWaitEvent(s->lanes[l], start_ev, 0), "wait");
+
+    for (int k = 0; k < SOGK_STATS_LEN; ++k) h_stats[k] = 0;
+    std::vector<int64_t> chunk_stats(size_t(nchunks) * SOGK_STATS_LEN, 0);
+    int64_t base = 0;
+    bool fits = true;
+    int rc = SOGK_OK;
+    // pass 1 of chunk c (upload, count, scan, stats download) on lane c % kLanes
+    auto issue_count = [&](int64_t c) -> int {
+        cudaStream_t L = s->lanes[c % kLanes];
+        const int64_t r0 = c * chunk, m = std::min(chunk, n - r0);
+        CK(cudaMemcpyAsync(d_rays + 8 * r0, h_rays + 8 * r0, size_t(m) * 64, cudaMemcpyHostToDevice, L), "rays H2D");
+        const int st = count_impl(s, d_rays + 8 * r0, nullptr, 0, m, d_packed + 2 * r0,
+                                  d_stats + c * SOGK_STATS_LEN, h_status ? d_status + r0 : nullptr,
+                                  h_counters ? d_ctr + 3 * r0 : nullptr, L);
+        if (st) return st;
+        int64_t* hs = s->h_chunk_stats + (c % 64) * SOGK_STATS_LEN;
+        CK(cudaMemcpyAsync(hs, d_stats + c * SOGK_STATS_LEN, SOGK_STATS_LEN * 8, cudaMemcpyDeviceToHost, L), "stats D2H");
+        CK(cudaEventRecord(s->lane_ev[c % kLanes], L), "event");
+        return SOGK_OK;
+    };
+    // pass 2 of chunk c (global offsets, write, downloads) once its total is known
+    auto issue_write = [&](int64_t c) -> int {
+        cudaStream_t L = s->lanes[c % kLanes];
+        CK(cudaEventSynchronize(s->lane_ev[c % kLanes]), "count sync");
+        const int64_t r0 = c * chunk, m = std::min(chunk, n - r0);
+        const int64_t* hs = s->h_chunk_stats + (c % 64) * SOGK_STATS_LEN;
+        for (int k = 0; k < SOGK_STATS_LEN; ++k) chunk_stats[size_t(c) * SOGK_STATS_LEN + k] = hs[k];
+        const int64_t tot = hs[SOGK_STAT_TOTAL_SAMPLES];
+        CK(launch_add_offset(d_packed + 2 * r0, m, base, L), "offsets");
+        if (fits && base + tot <= capacity) {
+            if (tot > 0) {
+                const int st = write_impl(s, d_rays + 8 * r0, nullptr, 0, m, d_packed + 2 * r0,
+                                          ray_index_base + r0, d_ts, h_t_ends ? d_te : nullptr,
+                                          h_ray_indices ? d_ri : nullptr, h_cells ? d_ce : nullptr,
+                                          h_levels ? d_lv : nullptr, L);
+                if (st) return st;
+                const size_t o = size_t(base), tb = size_t(tot);
+                if (h_t_starts) CK(cudaMemcpyAsync(h_t_starts + o, d_ts + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_t_ends) CK(cudaMemcpyAsync(h_t_ends + o, d_te + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_ray_indices) CK(cudaMemcpyAsync(h_ray_indices + o, d_ri + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_cells) CK(cudaMemcpyAsync(h_cells + o, d_ce + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_levels) CK(cudaMemcpyAsync(h_levels + o, d_lv + o, tb, cudaMemcpyDeviceToHost, L), "D2H");
+            }
+        } else {
+            fits = false;
+        }
+        CK(cudaMemcpyAsync(h_packed_info + 2 * r0, d_packed + 2 * r0, size_t(m) * 16, cudaMemcpyDeviceToHost, L), "D2H");
+        if (h_status) CK(cudaMemcpyAsync(h_status + r0, d_status + r0, size_t(m), cudaMemcpyDeviceToHost, L), "D2H");
+        if (h_counters) CK(cudaMemcpyAsync(h_counters + 3 * r0, d_ctr + 3 * r0, size_t(m) * 12, cudaMemcpyDeviceToHost, L), "D2H");
+        base += tot;
+        return SOGK_OK;
+    };
+    for (int64_t c = 0; c < nchunks && rc == SOGK_OK; ++c) {
+        rc = issue_count(c);
+        if (rc == SOGK_OK && c > 0) rc = issue_write(c - 1);
+        if (c + 1 == nchunks && rc == SOGK_OK) rc = issue_write(c);
+    }
+    for (int l = 0; l < kLanes; ++l) CK(cudaStreamSynchronize(s->lanes[l]), "pipeline sync");
     if (rc) return rc;
-    CK(cudaMemcpyAsync(h_stats, d_stats, SOGK_STATS_LEN * 8, cudaMemcpyDeviceToHost, st), "stats D2H");
-    CK(cudaStreamSynchronize(st), "count sync");
-    const int64_t total = h_stats[SOGK_STAT_TOTAL_SAMPLES];
-    const bool fits = total <= capacity;
-    if (fits && total > 0) {
-        rc = sogk_sample_write(s, d_rays, n, d_packed, ray_index_base, d_ts, h_t_ends ? d_te : nullptr,
-                               h_ray_indices ? d_ri : nullptr, h_cells ? d_ce : nullptr,
-                               h_levels ? d_lv : nullptr, stream);
-        if (rc) return rc;
-        const size_t tb = size_t(total);
-        if (h_t_starts) CK(cudaMemcpyAsync(h_t_starts, d_ts, tb * 8, cudaMemcpyDeviceToHost, st), "D2H");
-        if (h_t_ends) CK(cudaMemcpyAsync(h_t_ends, d_te, tb * 8, cudaMemcpyDeviceToHost, st), "D2H");
-        if (h_ray_indices) CK(cudaMemcpyAsync(h_ray_indices, d_ri, tb * 4, cudaMemcpyDeviceToHost, st), "D2H");
-        if (h_cells) CK(cudaMemcpyAsync(h_cells, d_ce, tb * 4, cudaMemcpyDeviceToHost, st), "D2H");
-        if (h_levels) CK(cudaMemcpyAsync(h_levels, d_lv, tb, cudaMemcpyDeviceToHost, st), "D2H");
-    }
-    if (n > 0) {
-        CK(cudaMemcpyAsync(h_packed_info, d_packed, size_t(n) * 16, cudaMemcpyDeviceToHost, st), "D2H");
-        if (h_status) CK(cudaMemcpyAsync(h_status, d_status, size_t(n), cudaMemcpyDeviceToHost, st), "D2H");
-        if (h_counters) CK(cudaMemcpyAsync(h_counters, d_ctr, size_t(n) * 12, cudaMemcpyDeviceToHost, st), "D2H");
-    }
-    CK(cudaStreamSynchronize(st), "write sync");
+    for (int64_t c = 0; c < nchunks; ++c)
+        for (int k = 0; k < SOGK_STATS_LEN; ++k) {
+            if (k == SOGK_STAT_TOTAL_SAMPLES || k == SOGK_STAT_INVALID_RAYS || k == SOGK_STAT_UNDEFINED_RAYS ||
+                k == SOGK_STAT_ANALYZER_LOOKUPS || k == SOGK_STAT_ANALYZER_STEPS ||
+                k == SOGK_STAT_KERNEL_LOOKUPS || k == SOGK_STAT_SLAB_OVERFLOW_RAYS)
+                h_stats[k] += chunk_stats[size_t(c) * SOGK_STATS_LEN + k];
+        }
     if (!fits) return fail(SOGK_INSUFFICIENT_CAPACITY, "output capacity below the sample total");
     return SOGK_OK;
 }

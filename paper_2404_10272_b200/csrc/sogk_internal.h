@@ -73,6 +73,9 @@ cudaError_t launch_render_composite(const Variant& v, const SamplerDev& s, const
                                     const int64_t* packed, const SlabDev& S, double* result,
                                     uint8_t* rgb8, cudaStream_t st);
 
+// packed_info[r].offset += base for r < n
+cudaError_t launch_add_offset(int64_t* packed, int64_t n, int64_t base, cudaStream_t st);
+
 cudaError_t launch_raygen(const CameraDev& cam, int64_t first, int64_t n, double* rays,
                           cudaStream_t st);
 

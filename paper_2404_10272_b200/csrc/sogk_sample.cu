@@ -723,6 +723,17 @@ cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* ra
     }
 }
 
+__global__ void add_offset_kernel(int64_t* packed, int64_t n, int64_t base) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) packed[2 * i] += base;
+}
+
+cudaError_t launch_add_offset(int64_t* packed, int64_t n, int64_t base, cudaStream_t st) {
+    if (n <= 0 || base == 0) return cudaSuccess;
+    add_offset_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(packed, n, base);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_raygen(const CameraDev& cam, int64_t first, int64_t n, double* rays,
                           cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
