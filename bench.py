@@ -280,52 +280,73 @@ def run_gpu(args):
             wl.fill_rays(rays[s][o], s, o, rank, world)
     torch.cuda.synchronize()
 
-    packed = [torch.empty((nr, 2), dtype=torch.int64, device=dev) for _ in range(n_obj)]
-    stats = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(n_obj)]
-    # --- sizing pass (untimed): totals of every (step, object) -> output capacity per object
+    # parts: the units one count/write pair processes -- one per object, or, for single-object
+    # configs on several streams, one contiguous ray range per stream (each its own packed batch)
+    if n_obj == 1 and args.streams > 1:
+        cut = [nr * i // args.streams for i in range(args.streams + 1)]
+        parts = [(0, cut[i], cut[i + 1]) for i in range(args.streams)]
+    else:
+        parts = [(o, 0, nr) for o in range(n_obj)]
+    n_parts = len(parts)
+
+    def prays(s_, pi):
+        o, a, b = parts[pi]
+        return rays[s_][o][a:b]
+
+    packed = [torch.empty((b - a, 2), dtype=torch.int64, device=dev) for _, a, b in parts]
+    stats = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in parts]
+    # --- sizing pass (untimed): totals of every (step, part) -> output capacity per part
     totals = {}
-    cap = [0] * n_obj
+    cap = [0] * n_parts
     for vname, smp in samplers.items():
         for s in range(steps_total):
-            for o in range(n_obj):
-                smp[o].count(rays[s][o], packed_info=packed[o], stats=stats[o])
-                tot = int(stats[o][0].item())
-                totals[(vname, s, o)] = tot
-                cap[o] = max(cap[o], tot)
+            for pi, (o, a, b) in enumerate(parts):
+                smp[o].count(prays(s, pi), packed_info=packed[pi], stats=stats[pi])
+                tot = int(stats[pi][0].item())
+                totals[(vname, s, pi)] = tot
+                cap[pi] = max(cap[pi], tot)
     outs = []
-    for o in range(n_obj):
-        c = max(1, cap[o])
+    for pi in range(n_parts):
+        c = max(1, cap[pi])
         outs.append(dict(t_starts=torch.empty(c, dtype=torch.float64, device=dev),
                          t_ends=torch.empty(c, dtype=torch.float64, device=dev),
                          ray_indices=torch.empty(c, dtype=torch.int32, device=dev),
                          cells=torch.empty(c, dtype=torch.int32, device=dev)))
-    # hit rays per (step, object) for the write kernel's algorithmic bytes
+    # object totals (the e2e leg's capacities)
+    obj_cap = [0] * n_obj
+    for vname in samplers:
+        for s in range(steps_total):
+            per = [0] * n_obj
+            for pi, (o, a, b) in enumerate(parts):
+                per[o] += totals[(vname, s, pi)]
+            for o in range(n_obj):
+                obj_cap[o] = max(obj_cap[o], per[o])
+    # hit rays per (step, part) for the write kernel's algorithmic bytes
     hits = {}
     for s in range(steps_total):
-        for o in range(n_obj):
+        for pi, (o, a, b) in enumerate(parts):
             smp = samplers[next(iter(samplers))][o]
-            smp.count(rays[s][o], packed_info=packed[o], stats=stats[o])
-            hits[(s, o)] = int((packed[o][:, 1] > 0).sum().item())
+            smp.count(prays(s, pi), packed_info=packed[pi], stats=stats[pi])
+            hits[(s, pi)] = int((packed[pi][:, 1] > 0).sum().item())
 
     stream = torch.cuda.current_stream()
     results = {}
     for vname, smp in samplers.items():
         def one_step(s, ev=None):
-            for o in range(n_obj):
+            for pi, (o, a, b) in enumerate(parts):
                 if ev is not None:
-                    ev[o][0].record(stream)
-                smp[o].count(rays[s][o], packed_info=packed[o], stats=stats[o])
+                    ev[pi][0].record(stream)
+                smp[o].count(prays(s, pi), packed_info=packed[pi], stats=stats[pi])
                 if ev is not None:
-                    ev[o][1].record(stream)
-                o_ = outs[o]
-                smp[o].write(rays[s][o], packed[o], totals[(vname, s, o)], ray_index_base=0,
-                             out=o_, cells=True, levels=False)
+                    ev[pi][1].record(stream)
+                smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=a,
+                             out=outs[pi], cells=True, levels=False)
                 if ev is not None:
-                    ev[o][2].record(stream)
+                    ev[pi][2].record(stream)
 
         for s in range(args.warmup):
             one_step(s)
-        evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_obj)]
+        evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_parts)]
                for _ in range(args.steps)]
         if world > 1:
             dist.barrier()
@@ -341,11 +362,49 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
         ms = t0.elapsed_time(t1)
-        count_ms = sum(evs[k][o][0].elapsed_time(evs[k][o][1]) for k in range(args.steps) for o in range(n_obj))
-        write_ms = sum(evs[k][o][1].elapsed_time(evs[k][o][2]) for k in range(args.steps) for o in range(n_obj))
-        samples = sum(totals[(vname, args.warmup + k, o)] for k in range(args.steps) for o in range(n_obj))
-        nhit = sum(hits[(args.warmup + k, o)] for k in range(args.steps) for o in range(n_obj))
-        results[vname] = dict(ms=ms, count_ms=count_ms, write_ms=write_ms, samples=samples,
+        ms_serial = ms
+        if args.streams > 1:
+            # the same steps with objects spread over `streams` CUDA streams (each stream has
+            # its own pass-1 -> pass-2 workspace): one object's pass 2 (memory-bound) overlaps
+            # the next object's pass 1 (issue-bound); sizes are precomputed, no host sync
+            side = [torch.cuda.Stream(device=dev) for _ in range(args.streams)]
+
+            def step_overlapped(s):
+                for pi, (o, a, b) in enumerate(parts):
+                    st = side[pi % args.streams]
+                    smp[o].count(prays(s, pi), packed_info=packed[pi], stats=stats[pi], stream=st)
+                    smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=a,
+                                 out=outs[pi], cells=True, levels=False, stream=st)
+
+            for st in side:
+                st.wait_stream(stream)
+            for s in range(args.warmup):
+                step_overlapped(s)
+            for st in side:
+                stream.wait_stream(st)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            u0 = torch.cuda.Event(enable_timing=True)
+            u1 = torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clk:
+                u0.record(stream)
+                for st in side:
+                    st.wait_event(u0)
+                for k in range(args.steps):
+                    step_overlapped(args.warmup + k)
+                for st in side:
+                    stream.wait_stream(st)
+                u1.record(stream)
+                torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            ms = u0.elapsed_time(u1)
+        count_ms = sum(evs[k][pi][0].elapsed_time(evs[k][pi][1]) for k in range(args.steps) for pi in range(n_parts))
+        write_ms = sum(evs[k][pi][1].elapsed_time(evs[k][pi][2]) for k in range(args.steps) for pi in range(n_parts))
+        samples = sum(totals[(vname, args.warmup + k, pi)] for k in range(args.steps) for pi in range(n_parts))
+        nhit = sum(hits[(args.warmup + k, pi)] for k in range(args.steps) for pi in range(n_parts))
+        results[vname] = dict(ms=ms, ms_serial=ms_serial, count_ms=count_ms, write_ms=write_ms, samples=samples,
                               hit_rays=nhit, clocks=clk.summary())
 
     # --- render leg: render_frame fused (sample + composite per pixel, no sample arrays),
@@ -395,7 +454,7 @@ def run_gpu(args):
                 t.copy_(rays[s][o], non_blocking=False)
                 row.append(t)
             h_rays.append(row)
-        hcap = max(cap)
+        hcap = max(obj_cap)
         h_out = dict(packed_info=torch.empty((nr, 2), dtype=torch.int64, pin_memory=True).numpy(),
                      t_starts=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
                      t_ends=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
@@ -438,7 +497,7 @@ def run_gpu(args):
 
         e2e_s = timed(False)
         e2e_full_s = timed(True)
-        samples0 = sum(totals[(vname0, args.warmup + k, o)] for k in range(args.steps) for o in range(n_obj))
+        samples0 = sum(totals[(vname0, args.warmup + k, pi)] for k in range(args.steps) for pi in range(n_parts))
         e2e = dict(seconds=e2e_s, h2d=nr * 64 * n_obj,
                    d2h_per_run=samples0 * 8 / args.steps + nr * (16 + 12) * n_obj,
                    full_seconds=e2e_full_s, full_d2h=samples0 * 24 / args.steps + nr * 16 * n_obj)
@@ -460,7 +519,8 @@ def run_gpu(args):
 
     agg = {}
     for vname, r in results.items():
-        agg[vname] = dict(ms=rmax(r["ms"]), samples=rsum(r["samples"]), count_ms=r["count_ms"],
+        agg[vname] = dict(ms=rmax(r["ms"]), ms_serial=rmax(r["ms_serial"]), samples=rsum(r["samples"]),
+                          count_ms=r["count_ms"],
                           write_ms=r["write_ms"], hit_rays=r["hit_rays"], local_samples=r["samples"],
                           clocks=r["clocks"])
     if rank != 0:
@@ -480,7 +540,7 @@ def run_gpu(args):
     # pass 2 reads packed_info (16 B/ray) and writes the samples (24 B each).  The slabs
     # pass 1 hands to pass 2 (12 B/sample each way) are not algorithmic; ncu's DRAM bytes
     # (`traffic`, profiles/traffic_<cfg>.json) show them.
-    launches = args.steps * n_obj
+    launches = args.steps * n_parts
     nr_loc = nr * n_obj * args.steps
     write_bytes = nr_loc * 16 + h["local_samples"] * 24
     count_bytes = nr_loc * (64 + 16)
@@ -501,6 +561,12 @@ def run_gpu(args):
             traffic = json.load(open(tf))
         except Exception:
             traffic = {}
+    # the capture's launch covered `rays_per_launch` rays: scale to this run's launches
+    rays_per_launch_here = nr_loc / launches
+    tscale = rays_per_launch_here / traffic.get("rays_per_launch", rays_per_launch_here)
+    for key in ("pass1", "pass2"):
+        if key in traffic and traffic[key].get("dram_bytes_per_launch"):
+            traffic[key]["dram_bytes_per_launch"] = traffic[key]["dram_bytes_per_launch"] * tscale
     dom_key = "pass1" if dom is pass1 else "pass2"
     other_key = "pass2" if dom is pass1 else "pass1"
 
@@ -519,13 +585,14 @@ def run_gpu(args):
         "data": "synthetic (procedural occupancy grids from the reference generators, camera/probe rays)",
         "config": {"workload": args.config, "desc": wl.desc, "variant": "sparse+hdda+skip" if head == "hdda_skip" else head,
                    "rays_per_step": nr * n_obj * world, "objects": [o["label"] for o in wl.objects],
-                   "parallelism": f"rays sharded by view over {world} GPU(s)",
+                   "parallelism": f"rays sharded by view over {world} GPU(s), objects over {args.streams} stream(s)",
                    "l2": "inputs+outputs per step > 126 MB L2 (no flush)"},
         "samples_per_sec": samples_s,
         "samples_per_step": h["samples"] / args.steps,
         "variants": {k: {"rays_per_sec": total_rays / (v["ms"] / 1e3),
                          "samples_per_sec": v["samples"] / (v["ms"] / 1e3),
                          "ms_per_step": v["ms"] / args.steps,
+                         "ms_per_step_one_stream": v["ms_serial"] / args.steps,
                          "count_ms_per_step": v["count_ms"] / args.steps,
                          "write_ms_per_step": v["write_ms"] / args.steps} for k, v in agg.items()},
         "hdda_vs_dda_branch": (agg["dda_branch"]["ms"] / agg["hdda_skip"]["ms"]) if {"dda_branch", "hdda_skip"} <= agg.keys() else None,
@@ -692,6 +759,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="CUDA streams the step's objects are spread over (1: one stream)")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = {"cfg1": 200, "cfg2": 50, "cfg3": 200, "cfg4": 10}[args.config]

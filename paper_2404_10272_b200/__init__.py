@@ -525,11 +525,15 @@ class Sampler:
         torch = _torch()
         dev = rays.device
         o = out or {}
-        ts = o.get("t_starts", torch.empty(total, dtype=torch.float64, device=dev))
-        te = o.get("t_ends", torch.empty(total, dtype=torch.float64, device=dev))
-        ri = o.get("ray_indices", torch.empty(total, dtype=torch.int32, device=dev))
-        ce = o.get("cells", torch.empty(total, dtype=torch.int32, device=dev)) if cells else None
-        lv = o.get("levels", torch.empty(total, dtype=torch.uint8, device=dev)) if levels else None
+
+        def buf(key, dtype):  # the caller's buffer, or a new one (allocated only when missing)
+            return o[key] if key in o else torch.empty(total, dtype=dtype, device=dev)
+
+        ts = buf("t_starts", torch.float64)
+        te = buf("t_ends", torch.float64)
+        ri = buf("ray_indices", torch.int32)
+        ce = buf("cells", torch.int32) if cells else None
+        lv = buf("levels", torch.uint8) if levels else None
         if total == 0:  # nothing to write (empty tensors have no device address)
             return ts, te, ri, ce, lv
         _check(lib.sogk_sample_write(self._h, _ptr(rays), rays.shape[0], _ptr(packed_info),
