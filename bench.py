@@ -125,6 +125,7 @@ class Workload:
 
     def __init__(self, P, name: str):
         self.P, self.name = P, name
+        self.ray_order = 0
         base = P.GridTransform.cube(128, (-1.0, -1.0, -1.0), 2.0)
         self.cascade = False
         self.schedule = P.StepSchedule.constant(0.5 * base.voxel_size)
@@ -157,7 +158,9 @@ class Workload:
             self.objects = [dict(label="blobs s1 512^3", levels=[(t512, bits)], occupancy=occ)]
             self.schedule = P.StepSchedule.constant(0.5 * t512.voxel_size)
             self.n_probe = 1 << 24
-            self.desc = "512^3 blobs s1 (1.44%), 2^24 make_probe_rays, dt0 = half voxel"
+            self.ray_order = 1  # incoherent probe rays: pass 1 bins them (sogk_sampler_set_ray_order)
+            self.desc = ("512^3 blobs s1 (1.44%), 2^24 make_probe_rays, dt0 = half voxel; pass 1 "
+                         "processes the rays binned by grid entry cell and direction")
         else:
             raise SystemExit(f"unknown config {name}")
 
@@ -268,7 +271,8 @@ def run_gpu(args):
     for vname, (an, kk) in variants.items():
         samplers[vname] = [P.Sampler(grids[i][1] if an == P.Analyzer.hdda else
                                      dist_grids[i] if an == P.Analyzer.cd else grids[i][0], an, kk,
-                                     wl.schedule, cascade=wl.cascade) for i in range(n_obj)]
+                                     wl.schedule, cascade=wl.cascade, ray_order=wl.ray_order)
+                           for i in range(n_obj)]
 
     nr = wl.rays_per_object()
     steps_total = args.warmup + args.steps
@@ -407,6 +411,7 @@ def run_gpu(args):
         results[vname] = dict(ms=ms, ms_serial=ms_serial, count_ms=count_ms, write_ms=write_ms, samples=samples,
                               hit_rays=nhit, clocks=clk.summary())
 
+    P.release_workspaces()
     # --- render leg: render_frame fused (sample + composite per pixel, no sample arrays),
     # the paper's rendered-frames metric; one frame = one object's view
     render = None
@@ -443,6 +448,7 @@ def run_gpu(args):
 
     # --- e2e through the host C-ABI entry point (pinned host buffers, H2D/D2H timed)
     e2e = None
+    P.release_workspaces()  # the timing legs' per-stream workspaces
     if not args.no_e2e:
         smp = samplers[next(iter(samplers))]
         vname0 = next(iter(samplers))

@@ -168,6 +168,13 @@ int sogk_grid_destroy(sogk_grid* g);
 int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
                         const sogk_sampler_desc* desc, sogk_sampler** out);
 int sogk_sampler_destroy(sogk_sampler* s);
+/* Processing order of pass 1 for device ray buffers: 0 (default) as given; 1 binned by the
+ * cell where a ray enters the grid and its direction (counting sort on the device), for
+ * incoherent batches such as probe rays.  Outputs are identical either way. */
+int sogk_sampler_set_ray_order(sogk_sampler* s, int order);
+/* Frees every pass-1 -> pass-2 workspace (one per device and stream, kept between calls);
+ * after it, a write without a fresh count takes the exact cold path.  Synchronizes the device. */
+int sogk_release_workspaces(void);
 
 /* Pass 1 of run_sampler / run_cascade_sampler over a batch (sampling.hpp:166-196, 440-455):
  * per-ray sample counts, exclusive-scanned on the device into d_packed_info[n][2]

@@ -116,6 +116,8 @@ _SIGS = {
     "sogk_grid_destroy": (C.c_int, [_vp]),
     "sogk_sampler_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(_SamplerDesc), C.POINTER(_vp)]),
     "sogk_sampler_destroy": (C.c_int, [_vp]),
+    "sogk_sampler_set_ray_order": (C.c_int, [_vp, C.c_int]),
+    "sogk_release_workspaces": (C.c_int, []),
     "sogk_sample_count": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_write": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_count_camera": (C.c_int, [_vp, C.POINTER(_Camera), _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
@@ -490,7 +492,8 @@ class Sampler:
     """
 
     def __init__(self, levels: Sequence[_Grid], analyzer: int, kernel: int,
-                 schedule: StepSchedule, cascade: bool = False, spin_cap: int = 0):
+                 schedule: StepSchedule, cascade: bool = False, spin_cap: int = 0,
+                 ray_order: int = 0):
         levels = list(levels)
         self.levels = levels  # keep the grids alive
         self.analyzer, self.kernel, self.schedule = analyzer, kernel, schedule
@@ -500,6 +503,8 @@ class Sampler:
         h = C.c_void_p()
         _check(lib.sogk_sampler_create(arr, len(levels), C.byref(d), C.byref(h)), "sampler")
         self._h = h.value
+        if ray_order:  # pass 1 in binned order (incoherent rays); outputs unchanged
+            _check(lib.sogk_sampler_set_ray_order(self._h, ray_order), "ray order")
 
     def __del__(self):
         try:
@@ -594,6 +599,11 @@ class Sampler:
             _check(rc, "sample_host")
             tot = int(stats[STAT_TOTAL_SAMPLES])
             return PackedSamples(pi, ts[:tot], te[:tot], ri[:tot], ce[:tot], lv[:tot], stt, ct, stats)
+
+
+def release_workspaces():
+    """Free the pass-1 -> pass-2 workspaces (one per device and stream)."""
+    _check(lib.sogk_release_workspaces(), "release_workspaces")
 
 
 def make_sampler(grid_or_levels, analyzer: int, kernel: int, schedule: StepSchedule,

@@ -253,8 +253,9 @@ struct sogk_sampler {
     // (device, stream) it ran on, tagged with the sampler and the rays; a write on that stream
     // by the same sampler on the same rays uses them, anything else takes the exact cold path
     const uint64_t id = ++g_sampler_ids;
+    int ray_order = 0; // 1: pass 1 processes buffer rays binned by entry cell and direction
     int64_t slab_cap = 128; // C: run records per ray (SOGK_SLAB; 0 = resume-only)
-    double slab_budget = 24.0 * (1ull << 30); // bytes of slabs per workspace (SOGK_SLAB_BUDGET_GB)
+    double slab_budget = 8.0 * (1ull << 30); // bytes of slabs per workspace (SOGK_SLAB_BUDGET_GB)
 
     int64_t cap_for(int64_t n) const {
         // keep the slabs within the budget; a smaller slab only sends more rays to
@@ -268,7 +269,14 @@ struct sogk_sampler {
     //              run counts | run slabs]
     size_t need_bytes(int64_t n) const {
         const size_t e = size_t(n) * size_t(cap_for(n));
-        return scan_off(n) + al(resume_bytes(n)) + 2 * al(size_t(n) * 4) + e * sizeof(RunRec);
+        return scan_off(n) + al(resume_bytes(n)) + 2 * al(size_t(n) * 4) + al(e * sizeof(RunRec)) +
+               (ray_order ? bin_scratch_bytes(n) : 0);
+    }
+    // ray-binning scratch, after the slabs
+    void* bin_scratch(const Workspace* w, int64_t n) const {
+        const size_t e = size_t(n) * size_t(cap_for(n));
+        return static_cast<char*>(w->ptr) + scan_off(n) + al(resume_bytes(n)) + 2 * al(size_t(n) * 4) +
+               al(e * sizeof(RunRec));
     }
     // the (device, stream) workspace, grown to fit n rays and tagged for this count
     int claim_ws(int64_t n, void* stream, const void* rays, bool cam, int64_t first, Workspace** out) {
@@ -965,6 +973,20 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     return SOGK_OK;
 }
 
+int sogk_release_workspaces(void) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    CK(cudaDeviceSynchronize(), "release sync");
+    for (auto& kv : ws_registry()) cudaFree(kv.second.ptr);
+    ws_registry().clear();
+    return SOGK_OK;
+}
+
+int sogk_sampler_set_ray_order(sogk_sampler* s, int order) {
+    if (!s || (order != 0 && order != 1)) return fail(SOGK_INVALID_ARG, "ray order must be 0 or 1");
+    s->ray_order = order;
+    return SOGK_OK;
+}
+
 int sogk_sampler_destroy(sogk_sampler* s) {
     delete s;
     return SOGK_OK;
@@ -1004,8 +1026,11 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
     const SlabDev slab = s->slab(w, n);
+    uint32_t* perm = nullptr;
+    if (s->ray_order && !cam)
+        CK(launch_ray_binning(s->dev, d_rays, n, s->bin_scratch(w, n), &perm, S(stream)), "ray binning");
     CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
-                    d_status, d_counters, slab, S(stream)),
+                    d_status, d_counters, slab, S(stream), perm),
        "count launch");
     if (scan)
         CK(launch_scan(n, d_packed, d_stats, sogk_sampler::tiles(w),

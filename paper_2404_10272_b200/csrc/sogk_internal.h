@@ -39,7 +39,11 @@ struct SlabDev {
 cudaError_t launch_count(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, int64_t* packed,
                          int64_t* stats, uint8_t* status, int32_t* counters, const SlabDev& slab,
-                         cudaStream_t st);
+                         cudaStream_t st, const uint32_t* perm = nullptr); // perm: processing order
+// ray binning (opt-in): a processing order grouping rays by grid entry cell and direction
+size_t bin_scratch_bytes(int64_t n);
+cudaError_t launch_ray_binning(const SamplerDev& s, const double* rays, int64_t n, void* scratch,
+                               uint32_t** perm, cudaStream_t st);
 cudaError_t launch_scan(int64_t n, int64_t* packed, int64_t* stats, uint64_t* tiles,
                         unsigned int* ctr, cudaStream_t st);
 int64_t scan_tiles(int64_t n);

@@ -175,9 +175,10 @@ __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MIN
     count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
                  int32_t* __restrict__ counters, const SlabDev S) {
-    const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     Stats5 acc;
-    if (r < n) {
+    if (j < n) {
+        const int64_t r = src.id(j);
         const Ray ray = src.load(r);
         if (!ray_valid(ray)) {
             count_invalid(r, packed, status, counters, acc);
@@ -685,14 +686,14 @@ struct Launch {
 cudaError_t launch_count(const Variant& v, const SamplerDev& s, const double* rays,
                          const CameraDev* cam, int64_t first, int64_t n, int64_t* packed,
                          int64_t* stats, uint8_t* status, int32_t* counters, const SlabDev& slab,
-                         cudaStream_t st) {
+                         cudaStream_t st, const uint32_t* perm) {
     if (cam) {
         using L = Launch<RaysFromCamera>;
         const RaysFromCamera src{*cam, first};
         SOGK_DISPATCH(count, s, src, n, packed, stats, status, counters, slab, st);
     } else {
         using L = Launch<RaysFromBuffer>;
-        const RaysFromBuffer src{rays};
+        const RaysFromBuffer src{rays, perm};
         SOGK_DISPATCH(count, s, src, n, packed, stats, status, counters, slab, st);
     }
 }
@@ -721,6 +722,81 @@ cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* ra
         const RaysFromBuffer src{rays};
         SOGK_DISPATCH(write, s, src, n, packed, slab, base, o, st);
     }
+}
+
+// ---------------------------------------------------------------------------
+// ray binning (opt-in, SOGK ray order 1): pass 1 processes incoherent rays grouped by where
+// they enter the grid and where they head, so that a warp's rays walk nearby nodes in step.
+// Key: 16^3 cells of the entry point into the (outermost) grid box x 8^3 direction bins;
+// counting sort (histogram, scan, atomic scatter).  Only the processing order changes.
+// ---------------------------------------------------------------------------
+constexpr int kBinBits = 21;
+
+__device__ __forceinline__ uint32_t bin_key(const Ray& r, const GridDev& g) {
+    double lo[3], hi[3], te, tx;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = g.wmin[a];
+        hi[a] = g.wmin[a] + (double)g.res[a] * g.voxel;
+    }
+    uint32_t c[3] = {0, 0, 0};
+    if (clip_to_box(r, lo, hi, te, tx)) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double u = (r.o[a] + r.d[a] * te - lo[a]) / (hi[a] - lo[a]) * 16.0;
+            c[a] = (uint32_t)(u < 0.0 ? 0.0 : (u > 15.0 ? 15.0 : u));
+        }
+    }
+    uint32_t d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double u = (r.d[a] + 1.0) * 4.0;
+        d[a] = (uint32_t)(u < 0.0 ? 0.0 : (u > 7.0 ? 7.0 : u));
+    }
+    return (((c[0] * 16 + c[1]) * 16 + c[2]) << 9) | (d[0] << 6) | (d[1] << 3) | d[2];
+}
+
+__global__ void bin_count_kernel(const SamplerDev s, const double* rays, int64_t n, uint32_t* keys,
+                                 unsigned long long* hist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = bin_key(RaysFromBuffer{rays}.load(i), s.lv[s.n_levels - 1]);
+    keys[i] = k;
+    atomicAdd(hist + 2 * k + 1, 1ull);
+}
+
+__global__ void bin_scatter_kernel(int64_t n, const uint32_t* keys, unsigned long long* hist,
+                                   uint32_t* perm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    perm[atomicAdd(hist + 2 * keys[i], 1ull)] = (uint32_t)i;
+}
+
+size_t bin_scratch_bytes(int64_t n) {
+    const int64_t bins = int64_t(1) << kBinBits;
+    return size_t(n) * 8 + size_t(bins) * 16 + size_t(scan_tiles(bins)) * 8 + 256;
+}
+
+cudaError_t launch_ray_binning(const SamplerDev& s, const double* rays, int64_t n, void* scratch,
+                               uint32_t** perm_out, cudaStream_t st) {
+    const int64_t bins = int64_t(1) << kBinBits;
+    char* p = static_cast<char*>(scratch);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(p);
+    uint32_t* perm = keys + n;
+    int64_t* hist = reinterpret_cast<int64_t*>(p + size_t(n) * 8);
+    uint64_t* tiles = reinterpret_cast<uint64_t*>(hist + 2 * bins);
+    int64_t* stats = reinterpret_cast<int64_t*>(tiles + scan_tiles(bins) + 1);
+    cudaError_t e = cudaMemsetAsync(hist, 0, size_t(bins) * 16 + size_t(scan_tiles(bins)) * 8 + 256, st);
+    if (e != cudaSuccess) return e;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    bin_count_kernel<<<blocks, 256, 0, st>>>(s, rays, n, keys, reinterpret_cast<unsigned long long*>(hist));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = launch_scan(bins, hist, stats, tiles, reinterpret_cast<unsigned int*>(tiles + scan_tiles(bins)), st);
+    if (e != cudaSuccess) return e;
+    bin_scatter_kernel<<<blocks, 256, 0, st>>>(n, keys, reinterpret_cast<unsigned long long*>(hist), perm);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *perm_out = perm;
+    return cudaSuccess;
 }
 
 __global__ void add_offset_kernel(int64_t* packed, int64_t n, int64_t base) {

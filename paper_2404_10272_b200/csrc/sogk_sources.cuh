@@ -14,6 +14,9 @@ namespace sogk {
 // ---------------------------------------------------------------------------
 struct RaysFromBuffer {
     const double* rays;
+    const uint32_t* perm = nullptr; // processing order (ray binning), nullptr: as given
+    // the ray a thread of pass 1 processes: every output stays indexed by this id
+    __device__ __forceinline__ int64_t id(int64_t j) const { return perm ? (int64_t)__ldg(perm + j) : j; }
     __device__ __forceinline__ Ray load(int64_t i) const {
         const double2* p = reinterpret_cast<const double2*>(rays + 8 * i);
         const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3);
@@ -54,6 +57,7 @@ __device__ __forceinline__ Ray pixel_ray(const CameraDev& c, int64_t pix) {
 struct RaysFromCamera {
     CameraDev cam;
     int64_t first;
+    __device__ __forceinline__ int64_t id(int64_t j) const { return j; }
     __device__ __forceinline__ Ray load(int64_t i) const { return pixel_ray(cam, first + i); }
 };
 
