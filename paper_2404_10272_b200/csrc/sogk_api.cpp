@@ -220,7 +220,8 @@ struct sogk_sampler {
     cudaStream_t lanes[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
     int64_t* h_chunk_stats = nullptr;
-    // sogk_render_camera scratch: stats (256 B) | packed counts [n][2]
+    // sogk_render_camera scratch: stats (256 B) | packed [n][2] | rays [n][8] | t [T] | ray index [T] |
+    // shaded [T][4]
     void* rb = nullptr;
     size_t rb_bytes = 0;
 
@@ -235,19 +236,42 @@ struct sogk_sampler {
             cudaFreeHost(h_chunk_stats);
         }
     }
-    int ensure_render(int64_t n) {
-        const size_t need = size_t(n) * 16 + 256;
+    static size_t ral(size_t x) { return (x + 255) & ~size_t(255); }
+    int ensure_render(int64_t n, int64_t total) {
+        const size_t need = 256 + ral(size_t(n) * 16) + ral(size_t(n) * 64) + ral(size_t(total) * 8) +
+                            ral(size_t(total) * 4) + size_t(total) * 32;
         if (need > rb_bytes) {
-            cudaFree(rb);
-            rb = nullptr;
-            rb_bytes = 0;
-            CK(cudaMalloc(&rb, need), "render scratch");
+            void* nb = nullptr;
+            CK(cudaMalloc(&nb, need), "render scratch");
+            if (rb) { // keep stats + packed (pass 1 already wrote them)
+                cudaError_t e = cudaMemcpy(nb, rb, std::min(rb_bytes, 256 + ral(size_t(n) * 16)),
+                                           cudaMemcpyDeviceToDevice);
+                cudaFree(rb);
+                if (e != cudaSuccess) {
+                    cudaFree(nb);
+                    rb = nullptr;
+                    rb_bytes = 0;
+                    return cuda_fail(e, "render scratch");
+                }
+            }
+            rb = nb;
             rb_bytes = need;
         }
         return SOGK_OK;
     }
-    int64_t* render_stats() const { return static_cast<int64_t*>(rb); }
-    int64_t* render_packed() const { return reinterpret_cast<int64_t*>(static_cast<char*>(rb) + 256); }
+    char* rbp() const { return static_cast<char*>(rb); }
+    int64_t* render_stats() const { return reinterpret_cast<int64_t*>(rbp()); }
+    int64_t* render_packed() const { return reinterpret_cast<int64_t*>(rbp() + 256); }
+    double* render_rays(int64_t n) const { return reinterpret_cast<double*>(rbp() + 256 + ral(size_t(n) * 16)); }
+    double* render_ts(int64_t n, int64_t) const {
+        return reinterpret_cast<double*>(rbp() + 256 + ral(size_t(n) * 16) + ral(size_t(n) * 64));
+    }
+    int32_t* render_ri(int64_t n, int64_t total) const {
+        return reinterpret_cast<int32_t*>(reinterpret_cast<char*>(render_ts(n, total)) + ral(size_t(total) * 8));
+    }
+    void* render_shaded(int64_t n, int64_t total) const {
+        return reinterpret_cast<char*>(render_ri(n, total)) + ral(size_t(total) * 4);
+    }
 
     // pass 1 -> pass 2 handshake: the run slabs of a count live in the workspace of the
     // (device, stream) it ran on, tagged with the sampler and the rays; a write on that stream
@@ -1229,19 +1253,30 @@ int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_came
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
     if (!camera_range_ok(cam, first_pixel, n)) return fail(SOGK_INVALID_ARG, "pixel outside image");
     if (!d_result && !d_rgb8) return fail(SOGK_INVALID_ARG, "NULL device buffer");
-    int st = s->ensure_render(n);
+    int st = s->ensure_render(n, 0);
     if (st) return st;
     int64_t* stats = d_stats ? d_stats : s->render_stats();
-    // pass 1 on the camera rays: counts, counters, samples into the slabs (no scan needed)
-    st = count_impl(s, nullptr, cam, first_pixel, n, s->render_packed(), stats, nullptr, nullptr,
-                    stream, /*scan=*/false);
+    // pass 1 + scan on the camera rays (rays generated in registers)
+    st = count_impl(s, nullptr, cam, first_pixel, n, s->render_packed(), stats, nullptr, nullptr, stream);
     if (st) return st;
     if (n == 0) return SOGK_OK;
-    CK(launch_render_composite(s->v, s->dev, scene->dev, to_dev(*cam), first_pixel, n,
-                               s->render_packed(),
-                               s->slab(s->owned_ws(stream, nullptr, true, first_pixel, n), n), d_result,
-                               d_rgb8, S(stream)),
-       "render launch");
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, stats + SOGK_STAT_TOTAL_SAMPLES, 8, cudaMemcpyDeviceToHost, S(stream)), "total D2H");
+    CK(cudaStreamSynchronize(S(stream)), "count sync");
+    st = s->ensure_render(n, total);
+    if (st) return st;
+    // pass 2 (t_starts, ray_indices), the ray buffer for shading, then shade + accumulate
+    if (total > 0) {
+        st = write_impl(s, nullptr, cam, first_pixel, n, s->render_packed(), 0, s->render_ts(n, total),
+                        nullptr, s->render_ri(n, total), nullptr, nullptr, stream);
+        if (st) return st;
+    }
+    const CameraDev cd = to_dev(*cam);
+    CK(launch_raygen(cd, first_pixel, n, s->render_rays(n), S(stream)), "raygen");
+    CK(launch_shade_accumulate(s->v, s->dev, scene->dev, s->render_rays(n), n, s->render_packed(),
+                               s->render_ts(n, total), s->render_ri(n, total), total, 0,
+                               s->render_shaded(n, total), d_result, d_rgb8, S(stream)),
+       "render shade");
     return SOGK_OK;
 }
 

@@ -71,11 +71,14 @@ struct SceneDev { // sog::AnalyticScene in HBM
 cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
                              const double* rays, int64_t n, const int64_t* packed, const double* ts,
                              double* result, uint8_t* rgb8, cudaStream_t st);
-// after launch_count on the camera rays: composite every ray from its slab (+ overflow tail)
-cudaError_t launch_render_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
-                                    const CameraDev& cam, int64_t first, int64_t n,
-                                    const int64_t* packed, const SlabDev& S, double* result,
+// frame compositing after pass 1 + scan + gather: per-sample shading (32 B each into
+// `shaded`), then the per-ray front-to-back sums
+cudaError_t launch_shade_accumulate(const Variant& v, const SamplerDev& s, const SceneDev& sc,
+                                    const double* rays, int64_t n, const int64_t* packed,
+                                    const double* ts, const int32_t* ri, int64_t total,
+                                    int64_t ray_index_base, void* shaded, double* result,
                                     uint8_t* rgb8, cudaStream_t st);
+
 
 // packed_info[r].offset += base for r < n
 cudaError_t launch_add_offset(int64_t* packed, int64_t n, int64_t base, cudaStream_t st);

@@ -2,13 +2,12 @@
 //
 // composite_kernel: composite_detailed (render.hpp:97-118) for every ray of a packed batch,
 //   one thread per ray over its contiguous samples.
-// render (sogk_render_camera): render_frame's per-pixel work (bench.hpp:424-461) as
-//   pass 1 (count_kernel on camera rays, samples into the per-ray slabs) followed by
-//   composite_slab_kernel, which composites each ray straight from its slab row: no scan, no
-//   packed sample arrays.  Shading (a loop over every primitive per sample) dominates; done
-//   in its own kernel the lanes of a warp shade in step, where interleaving it with the
-//   divergent traversal loop measured 4x slower.  Rays whose samples overflowed the slab are
-//   finished by render_tail_kernel (slab part, then the resumed traversal, composited).
+// render (sogk_render_camera): render_frame's per-pixel work (bench.hpp:424-461) as pass 1 +
+//   scan + pass 2 on the camera rays, then shade_kernel (per sample, all samples of the frame
+//   in parallel) and accumulate_kernel (per ray, the reference's sequential sums).  Shading (a
+//   loop over the candidate primitives and an exp per sample) dominates; interleaved with the
+//   divergent traversal loop it ran 4x slower, and thread-per-ray compositing made every warp
+//   wait on its longest ray.
 //
 // FP64 with the reference's operation order (Ray::at, density/emission sums in primitive
 // order, Vec3 operators); exp() is CUDA's (≤ 1 ulp), not glibc's, so results match the CPU
@@ -142,90 +141,86 @@ __global__ void __launch_bounds__(kRenderBlock)
     comp.store(r, result, rgb8);
 }
 
-// composite from the run slabs of pass 1 (rays whose runs all fit)
+// ---------------------------------------------------------------------------
+// render in three data-parallel steps after pass 1 + scan + gather (t_starts, ray_indices):
+//   shade_kernel:      per sample (all samples of the frame in parallel): alpha and the
+//                      emission colour (emission_at(p) = e / sigma); sigma <= 0 marked skip
+//   accumulate_kernel: per ray, the reference's sequential front-to-back sums over them
+// The arithmetic is the compositor's, operation for operation, so frames are bit-identical
+// to composite_kernel's; shading no longer waits on the longest ray of a warp.
+// ---------------------------------------------------------------------------
 template <int SCH>
-__device__ __forceinline__ long long composite_runs(Compositor<SCH>& comp, const SceneDev& sc,
-                                                    const Ray& ray, const SamplerDev& s,
-                                                    const RunRec* row, int nr, long long fill) {
-    for (int j = 0; j < nr; ++j) {
-        const RunRec a = row[j];
-        const long long start = a.sl & kRunStartMax;
-        const long long end = j + 1 < nr ? (long long)(row[j + 1].sl & kRunStartMax) : fill;
-        double t = a.first;
-        for (long long k = start; k < end; ++k) {
-            comp.add(sc, ray, s, t);
-            t = t + ladder_step<SCH>(t, s.dt0, s.growth);
-        }
+__global__ void __launch_bounds__(kRenderBlock)
+    shade_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const double* rays,
+                 int64_t total, const int64_t* __restrict__ packed, const double* __restrict__ ts,
+                 const int32_t* __restrict__ ri, int64_t ray_index_base,
+                 double4* __restrict__ shaded) {
+    const int64_t e = (int64_t)blockIdx.x * kRenderBlock + threadIdx.x;
+    if (e >= total) return;
+    const int64_t r = __ldg(ri + e) - ray_index_base;
+    const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
+    const double t = __ldg(ts + e);
+    // samples[i + 1] - t, or sched.step(t) for the ray's last sample (render.hpp:106)
+    const double dt = e + 1 < pi.x + pi.y ? __ldg(ts + e + 1) - t : ladder_step<SCH>(t, s.dt0, s.growth);
+    const Ray ray = RaysFromBuffer{rays}.load(r);
+    double p[3], em[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p[a] = ray.o[a] + ray.d[a] * t; // Ray::at (ray.hpp:35)
+    const double sigma = scene_at(sc, p, em);
+    double4 out;
+    if (sigma <= 0.0) {
+        out = make_double4(-1.0, 0.0, 0.0, 0.0); // skipped (render.hpp:109)
+    } else {
+        out = make_double4(1.0 - exp(-sigma * dt), em[0] / sigma, em[1] / sigma, em[2] / sigma);
     }
-    return fill;
+    shaded[e] = out;
 }
 
-template <int SCH, class Src>
 __global__ void __launch_bounds__(kRenderBlock)
-    composite_slab_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const Src src,
-                          int64_t n, const int64_t* __restrict__ packed, const SlabDev S,
-                          double* __restrict__ result, uint8_t* __restrict__ rgb8) {
+    accumulate_kernel(const SceneDev sc, int64_t n, const int64_t* __restrict__ packed,
+                      const double4* __restrict__ shaded, double* __restrict__ result,
+                      uint8_t* __restrict__ rgb8) {
     const int64_t r = (int64_t)blockIdx.x * kRenderBlock + threadIdx.x;
     if (r >= n) return;
-    const long long cnt = __ldg(reinterpret_cast<const longlong2*>(packed) + r).y;
-    const int raw = cnt > 0 ? __ldg(S.nruns + r) : 0;
-    if (raw < 0) return; // overflowed: render_tail_kernel
-    const Ray ray = src.load(r);
-    Compositor<SCH> comp;
+    const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
+    Compositor<0> comp;
     comp.init();
-    composite_runs<SCH>(comp, sc, ray, s, S.runs + r * S.C, raw, cnt);
-    comp.finish(sc, ray, s);
+    for (long long k = 0; k < pi.y; ++k) {
+        const double4 v = shaded[pi.x + k];
+        if (v.x < 0.0) continue; // sigma <= 0
+        const double alpha = v.x;
+        const double w = comp.T * alpha;
+        comp.c[0] += v.y * w;
+        comp.c[1] += v.z * w;
+        comp.c[2] += v.w * w;
+        comp.ws += w;
+        comp.T *= 1.0 - alpha;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) comp.c[a] += sc.bg[a] * comp.T; // background * transmittance
     comp.store(r, result, rgb8);
 }
 
-// rays whose runs overflowed the slab: the slab part, then the traversal resumed at the
-// first event that did not fit, all composited in order
-template <int AN, bool CASC, bool BR, int SCH, class Src>
-__global__ void __launch_bounds__(kRenderBlock)
-    render_tail_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const Src src,
-                       const int64_t* __restrict__ packed, const SlabDev S,
-                       double* __restrict__ result, uint8_t* __restrict__ rgb8) {
-    const unsigned cnt = *S.ovf_ctr;
-    for (unsigned i = blockIdx.x * kRenderBlock + threadIdx.x; i < cnt; i += gridDim.x * kRenderBlock) {
-        const int64_t r = S.ovf_list[i];
-        const long long total = __ldg(reinterpret_cast<const longlong2*>(packed) + r).y;
-        Resume res = S.resume[r];
-        const long long fill = res.tag >> 8;
-        res.tag &= 255;
-        const Ray ray = src.load(r);
-        Compositor<SCH> comp;
-        comp.init();
-        long long done = composite_runs<SCH>(comp, sc, ray, s, S.runs + r * S.C,
-                                             S.nruns[r] & 0x7fffffff, fill);
-        RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
-        gen.init(ray, s);
-        gen.resume(s, res);
-        Run run;
-        while (done < total) {
-            const int st = gen.step(s, run);
-            if (st == 0) break;
-            if (st != 2) continue;
-            double t = run.first;
-            for (int k = 0; k < run.n && done < total; ++k, ++done) {
-                comp.add(sc, ray, s, t);
-                t = t + ladder_step<SCH>(t, s.dt0, s.growth);
-            }
-        }
-        comp.finish(sc, ray, s);
-        comp.store(r, result, rgb8);
+cudaError_t launch_shade_accumulate(const Variant& v, const SamplerDev& s, const SceneDev& sc,
+                                    const double* rays, int64_t n, const int64_t* packed,
+                                    const double* ts, const int32_t* ri, int64_t total,
+                                    int64_t ray_index_base, void* shaded, double* result,
+                                    uint8_t* rgb8, cudaStream_t st) {
+    if (total > 0) {
+        const unsigned blocks = (unsigned)((total + kRenderBlock - 1) / kRenderBlock);
+        if (v.linear)
+            shade_kernel<1><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, total, packed, ts, ri, ray_index_base,
+                                                            static_cast<double4*>(shaded));
+        else
+            shade_kernel<0><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, total, packed, ts, ri, ray_index_base,
+                                                            static_cast<double4*>(shaded));
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
+    accumulate_kernel<<<(unsigned)((n + kRenderBlock - 1) / kRenderBlock), kRenderBlock, 0, st>>>(
+        sc, n, packed, static_cast<const double4*>(shaded), result, rgb8);
+    return cudaGetLastError();
 }
-
-struct RenderLaunch {
-    template <int AN, bool CASC, bool BR, int SCH>
-    static cudaError_t tail(const SamplerDev& s, const SceneDev& sc, const RaysFromCamera& src,
-                            const int64_t* packed, const SlabDev& S, double* result, uint8_t* rgb8,
-                            unsigned grid, cudaStream_t st) {
-        render_tail_kernel<AN, CASC, BR, SCH, RaysFromCamera>
-            <<<grid, kRenderBlock, 0, st>>>(s, sc, src, packed, S, result, rgb8);
-        return cudaGetLastError();
-    }
-};
 
 cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
                              const double* rays, int64_t n, const int64_t* packed, const double* ts,
@@ -236,23 +231,6 @@ cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneD
     else
         composite_kernel<0><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, n, packed, ts, result, rgb8);
     return cudaGetLastError();
-}
-
-cudaError_t launch_render_composite(const Variant& v, const SamplerDev& s, const SceneDev& sc,
-                                    const CameraDev& cam, int64_t first, int64_t n,
-                                    const int64_t* packed, const SlabDev& S, double* result,
-                                    uint8_t* rgb8, cudaStream_t st) {
-    const RaysFromCamera src{cam, first};
-    const unsigned blocks = (unsigned)((n + kRenderBlock - 1) / kRenderBlock);
-    if (v.linear)
-        composite_slab_kernel<1, RaysFromCamera><<<blocks, kRenderBlock, 0, st>>>(s, sc, src, n, packed, S, result, rgb8);
-    else
-        composite_slab_kernel<0, RaysFromCamera><<<blocks, kRenderBlock, 0, st>>>(s, sc, src, n, packed, S, result, rgb8);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    const unsigned tg = blocks < 148u * 8u ? (blocks ? blocks : 1u) : 148u * 8u;
-    using L = RenderLaunch;
-    SOGK_DISPATCH(tail, s, sc, src, packed, S, result, rgb8, tg, st);
 }
 
 } // namespace sogk
