@@ -531,4 +531,31 @@ int ref_build_distance(const int32_t res[3], const double wmin[3], double voxel,
     return g.all_empty() ? 1 : 0;
 }
 
+// run_matrix (bench.hpp:514-553) + emit_csv / emit_json (bench.hpp:563-605) of the reference
+// on a small config; returns the bytes needed (json then csv, NUL-separated) or -1 if cap is short
+int64_t ref_run_matrix(int kind, uint64_t seed, double fraction, int resolution, int cascades,
+                       int sched_kind, int width, int height, int repetitions, char* out,
+                       int64_t cap) {
+    BenchConfig cfg;
+    cfg.kind = SceneKind(kind);
+    cfg.params.seed = seed;
+    if (fraction > 0.0) cfg.params.fraction = fraction;
+    cfg.resolution = resolution;
+    cfg.cascades = cascades;
+    cfg.schedule_kind = sched_kind == 0 ? StepSchedule::Kind::constant : StepSchedule::Kind::linear;
+    cfg.width = width;
+    cfg.height = height;
+    cfg.repetitions = repetitions;
+    cfg.validate();
+    const BenchReport rep = run_matrix(cfg);
+    const std::string j = emit_json(rep), c = emit_csv(rep);
+    const int64_t need = int64_t(j.size() + c.size() + 2);
+    if (need > cap) return -need;
+    std::memcpy(out, j.data(), j.size());
+    out[j.size()] = 0;
+    std::memcpy(out + j.size() + 1, c.data(), c.size());
+    out[need - 1] = 0;
+    return need;
+}
+
 } // extern "C"

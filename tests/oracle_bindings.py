@@ -277,6 +277,9 @@ class RefLib:
                                        _i64p]
         L.ref_composite.argtypes = [_dp, C.c_void_p, C.c_int64, _dp, C.c_int, _dp, C.c_int,
                                     C.c_double, C.c_double, _dp]
+        L.ref_run_matrix.restype = C.c_int64
+        L.ref_run_matrix.argtypes = [C.c_int, C.c_uint64, C.c_double, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int64]
         L.ref_time_sampler.restype = C.c_double
         L.ref_time_sampler.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_void_p, C.c_int, C.c_int,
                                        C.POINTER(C.c_int64)]
@@ -342,6 +345,19 @@ class RefLib:
         self.L.ref_render_frame(SCENE_KINDS[kind], seed, fraction, resolution, cascades, sched_kind,
                                 width, height, grid, analyzer, kernel, nt, rgb, st)
         return rgb.reshape(height, width, 3), int(st[0]), int(st[1]), int(st[2])
+
+    def run_matrix(self, kind, seed=1, fraction=0.0, resolution=32, cascades=1, sched_kind=0,
+                   width=32, height=24, repetitions=1):
+        """the reference run_matrix (bench.hpp:514-553) -> (emit_json text, emit_csv text)."""
+        cap = 1 << 16
+        while True:
+            buf = C.create_string_buffer(cap)
+            n = self.L.ref_run_matrix(SCENE_KINDS[kind], seed, fraction, resolution, cascades,
+                                      sched_kind, width, height, repetitions, buf, cap)
+            if n > 0:
+                j, c = buf.raw[:n - 1].split(b"\0", 1)
+                return j.decode(), c.decode()
+            cap = -n
 
     def camera_rays(self, pos=(1.9, 1.4, 2.3), target=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0),
                     vfov=42.0, width=160, height=120, t_far=1e6) -> np.ndarray:
