@@ -60,6 +60,37 @@ cudaError_t dalloc(T** p, size_t count) {
     return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
 }
 
+// Grid storage comes from the device's stream-ordered pool, which keeps freed blocks
+// (release threshold = max) so rebuilding a grid does not pay cudaMalloc / cudaFree page
+// mapping -- the reference's conversion times are plain heap allocations.  The pool is
+// trimmed by sogk_release_workspaces.
+cudaError_t retain_pool() {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && !done[dev]) {
+        cudaMemPool_t pool;
+        if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
+        uint64_t keep = UINT64_MAX;
+        if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess)
+            return e;
+        done[dev] = true;
+    }
+    return cudaSuccess;
+}
+
+template <class T>
+cudaError_t galloc(T** p, size_t count, cudaStream_t st) {
+    *p = nullptr;
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = retain_pool();
+    if (e != cudaSuccess) return e;
+    return cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), st);
+}
+
 struct RootEntry { // one record of the reference root map (sparse.hpp:143-150)
     int32_t origin[3];
     uint8_t kind; // 0 empty tile, 1 occupied tile, 2 internal
@@ -106,18 +137,28 @@ struct sogk_grid {
     mutable std::vector<int32_t> h_root;
     mutable int64_t leaf_count = 0;
 
-    ~sogk_grid() {
-        cudaFree(bits);
-        cudaFree(root);
-        cudaFree(child_mask);
-        cudaFree(value_mask);
-        cudaFree(prefix);
-        cudaFree(table);
-        cudaFree(leaves);
-        cudaFree(region_leaves);
-        cudaFree(total_leaves);
-        cudaFree(dist);
-        cudaFree(dist_any);
+    // build completion on the build stream: host reads (metadata, downloads, exports) wait on it
+    cudaEvent_t ready = nullptr;
+    cudaError_t mark(cudaStream_t st) {
+        cudaError_t e = ready ? cudaSuccess : cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+        return e == cudaSuccess ? cudaEventRecord(ready, st) : e;
+    }
+    cudaError_t wait_ready() const { return ready ? cudaEventSynchronize(ready) : cudaSuccess; }
+
+    ~sogk_grid() { // pool blocks (galloc); like cudaFree, wait for work that may still read them
+        void* ps[] = {bits, root, child_mask, value_mask, prefix, table, leaves, region_leaves,
+                      total_leaves, dist, dist_any};
+        bool any = false;
+        for (void* p : ps) any |= p != nullptr;
+        if (!any) return;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != device) cudaSetDevice(device);
+        cudaDeviceSynchronize();
+        for (void* p : ps)
+            if (p) cudaFreeAsync(p, 0);
+        if (cur != device) cudaSetDevice(cur);
+        if (ready) cudaEventDestroy(ready);
     }
 
     GridDev dev() const {
@@ -157,6 +198,7 @@ struct sogk_grid {
             meta_ready = true;
             return SOGK_OK;
         }
+        CK(wait_ready(), "build completion");
         h_root.resize(nreg);
         CK(cudaMemcpy(h_root.data(), root, nreg * sizeof(int32_t), cudaMemcpyDeviceToHost), "root D2H");
         uint32_t tl = 0;
@@ -402,7 +444,7 @@ static int create_dense(const sogk_transform* t, const uint8_t* bits, size_t nby
     g->t = *t;
     g->nbytes = nbytes;
     cudaGetDevice(&g->device);
-    cudaError_t e = dalloc(&g->bits, nbytes);
+    cudaError_t e = galloc(&g->bits, nbytes, S(stream));
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(g->bits, bits, nbytes,
                             host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, S(stream));
@@ -425,18 +467,18 @@ int sogk_grid_create_dense_device(const sogk_transform* t, const uint8_t* d_bits
     return create_dense(t, d_bits, nbytes, false, stream, out);
 }
 
-static cudaError_t alloc_vdb(sogk_grid* g) {
+static cudaError_t alloc_vdb(sogk_grid* g, cudaStream_t st) {
     for (int a = 0; a < 3; ++a) g->R[a] = (g->t.res[a] + 127) / 128;
     g->nreg = int64_t(g->R[0]) * g->R[1] * g->R[2];
     g->leaf_capacity = uint64_t(g->nreg) * 4096;
     cudaError_t e;
-    if ((e = dalloc(&g->root, g->nreg)) != cudaSuccess) return e;
-    if ((e = dalloc(&g->child_mask, g->nreg * 64)) != cudaSuccess) return e;
-    if ((e = dalloc(&g->value_mask, g->nreg * 64)) != cudaSuccess) return e;
-    if ((e = dalloc(&g->prefix, g->nreg * 64)) != cudaSuccess) return e;
-    if ((e = dalloc(&g->table, g->nreg * 4096)) != cudaSuccess) return e;
-    if ((e = dalloc(&g->region_leaves, g->nreg)) != cudaSuccess) return e;
-    if ((e = dalloc(&g->total_leaves, 1)) != cudaSuccess) return e;
+    if ((e = galloc(&g->root, g->nreg, st)) != cudaSuccess) return e;
+    if ((e = galloc(&g->child_mask, g->nreg * 64, st)) != cudaSuccess) return e;
+    if ((e = galloc(&g->value_mask, g->nreg * 64, st)) != cudaSuccess) return e;
+    if ((e = galloc(&g->prefix, g->nreg * 64, st)) != cudaSuccess) return e;
+    if ((e = galloc(&g->table, g->nreg * 4096, st)) != cudaSuccess) return e;
+    if ((e = galloc(&g->region_leaves, g->nreg, st)) != cudaSuccess) return e;
+    if ((e = galloc(&g->total_leaves, 1, st)) != cudaSuccess) return e;
     return cudaSuccess;
 }
 
@@ -451,8 +493,8 @@ int sogk_grid_build_vdb(const sogk_grid* d, void* stream, sogk_grid** out) {
     g->kind = SOGK_GRID_VDB;
     g->t = d->t;
     g->device = d->device;
-    cudaError_t e = alloc_vdb(g);
-    if (e == cudaSuccess) e = dalloc(&g->leaves, g->leaf_capacity * 8);
+    cudaError_t e = alloc_vdb(g, S(stream));
+    if (e == cudaSuccess) e = galloc(&g->leaves, g->leaf_capacity * 8, S(stream));
     if (e != cudaSuccess) {
         delete g;
         return cuda_fail(e, "vdb allocation");
@@ -469,6 +511,7 @@ int sogk_grid_build_vdb(const sogk_grid* d, void* stream, sogk_grid** out) {
     a.region_leaves = g->region_leaves;
     a.total_leaves = g->total_leaves;
     e = launch_vdb_build(a, S(stream));
+    if (e == cudaSuccess) e = g->mark(S(stream));
     if (e != cudaSuccess) {
         delete g;
         return cuda_fail(e, "vdb build launch");
@@ -490,12 +533,12 @@ int sogk_grid_build_distance(const sogk_grid* d, void* stream, sogk_grid** out) 
     g->device = d->device;
     const uint64_t n = voxel_count(d->t);
     int32_t* scratch = nullptr;
-    cudaError_t e = dalloc(&g->dist, n);
-    if (e == cudaSuccess) e = dalloc(&g->dist_any, 1);
-    if (e == cudaSuccess) e = dalloc(&scratch, n);
+    cudaError_t e = galloc(&g->dist, n, S(stream));
+    if (e == cudaSuccess) e = galloc(&g->dist_any, 1, S(stream));
+    if (e == cudaSuccess) e = galloc(&scratch, n, S(stream));
     if (e == cudaSuccess) e = launch_distance_build(d->dev(), g->dist, scratch, g->dist_any, S(stream));
-    if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream)); // before the scratch goes
-    cudaFree(scratch);
+    if (scratch) cudaFreeAsync(scratch, S(stream)); // stream-ordered: after the passes
+    if (e == cudaSuccess) e = g->mark(S(stream));
     if (e != cudaSuccess) {
         delete g;
         return cuda_fail(e, "distance build");
@@ -508,6 +551,7 @@ int sogk_grid_download_distance(const sogk_grid* g, int32_t* h_dist, size_t coun
                                 int32_t* all_empty) {
     if (!g || g->kind != SOGK_GRID_DISTANCE) return fail(SOGK_INVALID_ARG, "not a distance grid");
     const uint64_t n = voxel_count(g->t);
+    CK(g->wait_ready(), "build completion");
     if (h_dist) {
         if (count < n) return fail(SOGK_INSUFFICIENT_CAPACITY, "buffer smaller than the grid");
         CK(cudaMemcpy(h_dist, g->dist, n * sizeof(int32_t), cudaMemcpyDeviceToHost), "distance D2H");
@@ -870,8 +914,9 @@ int sogk_grid_load_sog1(const uint8_t* bytes, size_t len, void* stream, sogk_gri
     for (auto& x : dev_root)
         if (x == -3) x = kRootEmpty;
     g->leaf_capacity = leaves.size() / 8;
-    cudaError_t e = alloc_vdb(g);
-    if (e == cudaSuccess) e = dalloc(&g->leaves, std::max<size_t>(leaves.size(), 8));
+    // legacy stream: the synchronous uploads below are ordered after the allocations
+    cudaError_t e = alloc_vdb(g, nullptr);
+    if (e == cudaSuccess) e = galloc(&g->leaves, std::max<size_t>(leaves.size(), 8), nullptr);
     const uint32_t tl = uint32_t(leaves.size() / 8);
     if (e == cudaSuccess) e = cudaMemcpy(g->root, dev_root.data(), dev_root.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->child_mask, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice);
@@ -909,6 +954,7 @@ int sogk_grid_download_dense(const sogk_grid* g, uint8_t* h_bits, size_t nbytes)
         CK(cudaMemcpy(h_bits, g->bits, nbytes, cudaMemcpyDeviceToHost), "payload D2H");
         return SOGK_OK;
     }
+    CK(g->wait_ready(), "build completion");
     uint8_t* d = nullptr;
     CK(cudaMalloc(&d, nbytes), "to_dense scratch");
     cudaError_t e = launch_vdb_to_dense(g->dev(), d, int64_t(nbytes), nullptr);
@@ -1002,6 +1048,10 @@ int sogk_release_workspaces(void) {
     CK(cudaDeviceSynchronize(), "release sync");
     for (auto& kv : ws_registry()) cudaFree(kv.second.ptr);
     ws_registry().clear();
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolTrimTo(pool, 0); // grid blocks kept by the pool
     return SOGK_OK;
 }
 
