@@ -18,6 +18,7 @@ JSON line keys follow the driver contract; see DESIGN.md §Measurement for the r
 from __future__ import annotations
 
 import argparse
+from concurrent.futures import ThreadPoolExecutor
 import json
 import math
 import os
@@ -461,20 +462,30 @@ def run_gpu(args):
                 row.append(t)
             h_rays.append(row)
         hcap = max(obj_cap)
-        h_out = dict(packed_info=torch.empty((nr, 2), dtype=torch.int64, pin_memory=True).numpy(),
+        n_workers = max(1, min(args.e2e_workers, n_obj))
+
+        def host_outputs():  # pinned output buffers, one set per worker thread
+            o = dict(packed_info=torch.empty((nr, 2), dtype=torch.int64, pin_memory=True).numpy(),
                      t_starts=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
                      t_ends=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
                      ray_indices=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy(),
                      cells=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
                      stats=np.zeros(8, np.int64))
-        h_out["counters"] = torch.empty((nr, 3), dtype=torch.int32, pin_memory=True).numpy()
-        lib = P.lib
+            o["counters"] = torch.empty((nr, 3), dtype=torch.int32, pin_memory=True).numpy()
+            return o
 
-        def e2e_step(s, full):
+        h_outs = [host_outputs() for _ in range(n_workers)]
+        lib = P.lib
+        pool = ThreadPoolExecutor(n_workers) if n_workers > 1 else None
+
+        def e2e_objects(s, full, w):
             # full: the packed intervals (t_starts, t_ends, ray_indices, cells); otherwise what
             # the reference's run_sampler returns per ray (sampling.hpp:157-164): its sample
-            # buffer (packed t_starts + packed_info) and its three counters
-            for o in range(n_obj):
+            # buffer (packed t_starts + packed_info) and its three counters.  Worker w takes the
+            # objects o = w mod n_workers (independent samplers: each call is synchronous and
+            # pipelines its own chunks; ctypes drops the GIL, so the calls overlap)
+            h_out = h_outs[w]
+            for o in range(w, n_obj, n_workers):
                 rc = lib.sogk_sample_host(smp[o]._h, h_rays[s][o].data_ptr(), nr, 0, hcap,
                                           h_out["packed_info"].ctypes.data, h_out["t_starts"].ctypes.data,
                                           h_out["t_ends"].ctypes.data if full else None,
@@ -483,6 +494,13 @@ def run_gpu(args):
                                           None if full else h_out["counters"].ctypes.data,
                                           h_out["stats"].ctypes.data, stream.cuda_stream or None)
                 P._check(rc, "sample_host")
+
+        def e2e_step(s, full):
+            if pool is None:
+                e2e_objects(s, full, 0)
+            else:
+                for f in [pool.submit(e2e_objects, s, full, w) for w in range(n_workers)]:
+                    f.result()
 
         def timed(full):
             for s in range(args.warmup):
@@ -504,7 +522,9 @@ def run_gpu(args):
         e2e_s = timed(False)
         e2e_full_s = timed(True)
         samples0 = sum(totals[(vname0, args.warmup + k, pi)] for k in range(args.steps) for pi in range(n_parts))
-        e2e = dict(seconds=e2e_s, h2d=nr * 64 * n_obj,
+        if pool is not None:
+            pool.shutdown()
+        e2e = dict(seconds=e2e_s, h2d=nr * 64 * n_obj, workers=n_workers,
                    d2h_per_run=samples0 * 8 / args.steps + nr * (16 + 12) * n_obj,
                    full_seconds=e2e_full_s, full_d2h=samples0 * 24 / args.steps + nr * 16 * n_obj)
 
@@ -630,6 +650,7 @@ def run_gpu(args):
                        "api": "sogk_sample_host: pinned host rays in; out, what run_sampler returns per ray "
                               "(sampling.hpp:157-164): its samples (packed t_starts + packed_info) and "
                               "its three counters",
+                       "host_threads": e2e["workers"],
                        "full_intervals": {"value": total_rays / e2e["full_seconds"], "unit": "rays/s",
                                           "d2h_bytes_per_step": int(e2e["full_d2h"]),
                                           "outputs": "packed_info, t_starts, t_ends, ray_indices, cells"}}
@@ -763,6 +784,8 @@ def main():
     ap.add_argument("--variants", default="")
     ap.add_argument("--cpu-stride", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-workers", type=int, default=2,
+                    help="host threads issuing sogk_sample_host calls for different objects concurrently")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--streams", type=int, default=2,

@@ -54,7 +54,7 @@ OK, INVALID_ARG, CUDA_ERROR, OOM, INSUFFICIENT_CAPACITY, IO_ERROR, NO_DEVICE = r
 RAY_OK, RAY_INVALID, RAY_UNDEFINED = 0, 1, 2
 STATS_LEN = 8
 (STAT_TOTAL_SAMPLES, STAT_INVALID_RAYS, STAT_UNDEFINED_RAYS, STAT_ANALYZER_LOOKUPS,
- STAT_ANALYZER_STEPS, STAT_KERNEL_LOOKUPS) = range(6)
+ STAT_ANALYZER_STEPS, STAT_KERNEL_LOOKUPS, STAT_SLAB_OVERFLOW_RAYS) = range(7)
 
 
 class IoError(RuntimeError):
