@@ -595,6 +595,26 @@ def run_gpu(args):
             traffic[key]["dram_bytes_per_launch"] = traffic[key]["dram_bytes_per_launch"] * tscale
     dom_key = "pass1" if dom is pass1 else "pass2"
     other_key = "pass2" if dom is pass1 else "pass1"
+    # pass 1's real ceiling is instruction issue: warp instructions of one step's
+    # count_kernel launches (ncu, profiles/issue_<cfg>.json, tools/issue_probe.py) over the live
+    # pass-1 time, against 4 issue slots per SM per clock at the clock measured under load
+    issue = None
+    isf = os.path.join(ROOT, "profiles", f"issue_{args.config}.json")
+    if os.path.exists(isf) and head == "hdda_skip" and world == 1:
+        try:
+            ij = json.load(open(isf))
+            sm_mhz = (h["clocks"] or {}).get("sm_mhz") or 0
+            n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            ipeak = n_sm * 4 * sm_mhz * 1e6
+            iach = ij["pass1_warp_inst_per_step"] / (h["count_ms"] / args.steps / 1e3)
+            issue = {"bound": "issue", "kernel": "count_kernel (pass 1; time incl. scan_kernel)",
+                     "achieved": iach, "peak": ipeak, "unit": "warp-inst/s",
+                     "frac": iach / ipeak if ipeak else None,
+                     "warp_inst_per_step": ij["pass1_warp_inst_per_step"],
+                     "peak_basis": f"{n_sm} SMs x 4 schedulers x {sm_mhz} MHz (median SM clock under load)",
+                     "source": ij.get("source")}
+        except Exception as e:  # noqa: BLE001
+            issue = {"error": str(e)}
 
     line = {
         "metric": "rays/sec and samples/sec per B200 (and 8-GPU box), HDDA-VDB vs dense-DDA, % HBM roofline",
@@ -630,7 +650,8 @@ def run_gpu(args):
                              "(object 0), " + traffic.get("source", "no capture committed"),
                      "other_pass": {"kernel": other["kernel"], "achieved": gbs(other), "frac": gbs(other) / peak,
                                     "algorithmic_bytes_per_launch": other["bytes"] / launches,
-                                    "traffic": traffic.get(other_key, {}).get("dram_bytes_per_launch")}},
+                                    "traffic": traffic.get(other_key, {}).get("dram_bytes_per_launch")},
+                     "issue_ceiling": issue},
         "step_roofline": {"bytes_per_step": step_bytes / args.steps, "achieved_gbs": step_gbs,
                           "frac": step_gbs / peak,
                           "basis": "N_rays*(64+16) + N_samples*24 + VDB bytes (SURVEY §8d)"},

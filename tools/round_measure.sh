@@ -18,3 +18,4 @@ for V in hdda_skip dda_branch; do
   python tools/ncu_summary.py /tmp/${TAG}_full_$V.ncu-rep > gpurun_out/${TAG}_ncu_cfg2_$V.txt 2>&1
   ncu -i /tmp/${TAG}_full_$V.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_raw_cfg2_$V.csv 2>/dev/null
 done
+bash tools/issue_all.sh > gpurun_out/${TAG}_issue.txt 2>&1
