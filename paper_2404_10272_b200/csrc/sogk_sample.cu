@@ -727,10 +727,22 @@ cudaError_t launch_write(const Variant& v, const SamplerDev& s, const double* ra
 // ---------------------------------------------------------------------------
 // ray binning (opt-in, SOGK ray order 1): pass 1 processes incoherent rays grouped by where
 // they enter the grid and where they head, so that a warp's rays walk nearby nodes in step.
-// Key: 16^3 cells of the entry point into the (outermost) grid box x 8^3 direction bins;
+// Key: 8^3 cells of the entry point into the (outermost) grid box x 16^3 direction bins
+// (cfg4: 3 % faster than 16^3 x 8^3, 20 % faster than 32^3 x 4^3 -- direction coherence
+// matters more than entry position; SOGK_BIN_* select others for experiments);
 // counting sort (histogram, scan, atomic scatter).  Only the processing order changes.
 // ---------------------------------------------------------------------------
-constexpr int kBinBits = 21;
+#ifndef SOGK_BIN_CELL
+#define SOGK_BIN_CELL 3 // log2 entry-cell bins per axis
+#endif
+#ifndef SOGK_BIN_DIR
+#define SOGK_BIN_DIR 4 // log2 direction bins per axis
+#endif
+#ifndef SOGK_BIN_DIR_MAJOR
+#define SOGK_BIN_DIR_MAJOR 0 // key order: entry cell major (0) or direction major (1)
+#endif
+constexpr int kBinCell = SOGK_BIN_CELL, kBinDir = SOGK_BIN_DIR;
+constexpr int kBinBits = 3 * (kBinCell + kBinDir);
 
 __device__ __forceinline__ uint32_t bin_key(const Ray& r, const GridDev& g) {
     double lo[3], hi[3], te, tx;
@@ -739,21 +751,24 @@ __device__ __forceinline__ uint32_t bin_key(const Ray& r, const GridDev& g) {
         lo[a] = g.wmin[a];
         hi[a] = g.wmin[a] + (double)g.res[a] * g.voxel;
     }
+    constexpr double nc = double(1 << kBinCell), nd = double(1 << kBinDir);
     uint32_t c[3] = {0, 0, 0};
     if (clip_to_box(r, lo, hi, te, tx)) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const double u = (r.o[a] + r.d[a] * te - lo[a]) / (hi[a] - lo[a]) * 16.0;
-            c[a] = (uint32_t)(u < 0.0 ? 0.0 : (u > 15.0 ? 15.0 : u));
+            const double u = (r.o[a] + r.d[a] * te - lo[a]) / (hi[a] - lo[a]) * nc;
+            c[a] = (uint32_t)(u < 0.0 ? 0.0 : (u > nc - 1.0 ? nc - 1.0 : u));
         }
     }
     uint32_t d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const double u = (r.d[a] + 1.0) * 4.0;
-        d[a] = (uint32_t)(u < 0.0 ? 0.0 : (u > 7.0 ? 7.0 : u));
+        const double u = (r.d[a] + 1.0) * (0.5 * nd);
+        d[a] = (uint32_t)(u < 0.0 ? 0.0 : (u > nd - 1.0 ? nd - 1.0 : u));
     }
-    return (((c[0] * 16 + c[1]) * 16 + c[2]) << 9) | (d[0] << 6) | (d[1] << 3) | d[2];
+    const uint32_t ck = (((c[0] << kBinCell) | c[1]) << kBinCell) | c[2];
+    const uint32_t dk = (((d[0] << kBinDir) | d[1]) << kBinDir) | d[2];
+    return SOGK_BIN_DIR_MAJOR ? (dk << (3 * kBinCell)) | ck : (ck << (3 * kBinDir)) | dk;
 }
 
 __global__ void bin_count_kernel(const SamplerDev s, const double* rays, int64_t n, uint32_t* keys,
