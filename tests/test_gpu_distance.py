@@ -42,3 +42,36 @@ def test_distance_512(P):
     for z, y, x in rng.integers(0, 512, size=(40, 3)):
         ref = int(np.abs(pts - np.array([z, y, x])).max(axis=1).min())
         assert d[z, y, x] == ref
+
+
+@pytest.mark.parametrize("res", [(1500, 3, 4), (4, 1500, 3), (3, 4, 1500), (2047, 2, 2)])
+def test_distance_long_lines(P, oracle, res):
+    """Lines up to the 2047-voxel limit on each axis (shared-memory sizing of every pass)."""
+    t = P.GridTransform(res, (0.0, 0.0, 0.0), 1.0)
+    bits = P.random_grid(t, 11, 0.003)
+    d = P.build_distance(P.DenseGrid(t, bits))
+    want, ae = oracle.distance_field(host_grid(P, t, bits))
+    assert np.array_equal(d.distances(), want) and d.all_empty() == ae
+
+
+def test_builds_on_side_stream_then_read(P):
+    """Grid builds are stream-ordered (pool storage, no sync): host reads right after a build
+    on another stream wait for it (build-completion event), and rebuilt grids reusing pool
+    blocks give identical results."""
+    import torch
+
+    t = P.GridTransform.cube(128, (-1.0, -1.0, -1.0), 2.0)
+    bits, _ = P.generate_scene("shell", t, seed=1)
+    dense = P.DenseGrid(t, bits)
+    want_d = P.build_distance(dense).distances()
+    want_s = P.serialize_sparse(P.build_sparse(dense))
+    side = torch.cuda.Stream()
+    for _ in range(5):
+        with torch.cuda.stream(side):
+            g = P.build_distance(dense, stream=side)
+            v = P.build_sparse(dense, stream=side)
+        assert np.array_equal(g.distances(), want_d)
+        assert P.serialize_sparse(v) == want_s
+        del g, v
+    P.release_workspaces()  # trims the pool
+    assert np.array_equal(P.build_distance(dense).distances(), want_d)
