@@ -33,10 +33,26 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(1, os.path.join(ROOT, "tests"))  # oracle_bindings: CPU-baseline leg only
 
-from paper_2404_10272_b200.shard import broadcast_payload, view_of  # noqa: E402
+
+
+def _load_shard():
+    """paper_2404_10272_b200/shard.py loaded by path: importing it as a submodule would run the
+    package __init__ and load libsogk.so, which the reference arm must not do."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "_sogk_shard", os.path.join(ROOT, "paper_2404_10272_b200", "shard.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+_shard = _load_shard()
+broadcast_payload, shard_range, view_of = _shard.broadcast_payload, _shard.shard_range, _shard.view_of
 
 CAM_POS = (1.9, 1.4, 2.3)
 N_VIEWS = 200
+METRIC = "rays/sec and samples/sec per B200 (and 8-GPU box), HDDA-VDB vs dense-DDA, % HBM roofline"
 
 # cfg 2: 8 procedural 128^3 objects of varying sparsity (SURVEY §8d)
 CFG2_OBJECTS = [
@@ -49,170 +65,183 @@ CFG2_OBJECTS = [
     ("sponge", dict(seed=1)),
     ("random", dict(seed=1, fraction=0.02)),
 ]
+DESC = {
+    "cfg1": "single-level 128^3 shell s1, 800x800 bench camera, dt0 = half voxel",
+    "cfg2": ("8 procedural 128^3 objects (shell s1, shell s2 n256, blobs s1..s4 n6..48, sponge s1, "
+             "random 2%), 800x800 orbit views, dt0 = half voxel"),
+    "cfg3": "4-level 128^3 blobs s1 cascade, 1297x840 bench camera, linear dt0=2^-7 growth 1/256",
+    "cfg4": ("512^3 blobs s1 (1.44%), 2^24 make_probe_rays, dt0 = half voxel; pass 1 processes the "
+             "rays binned by grid entry cell and direction"),
+}
 
 
-def orbit_camera(P, view: int, width=800, height=800):
+def orbit_pos(view: int):
     """View v of the orbit: the bench pose rotated about +y by 2*pi*v/200 (v = 0 is cfg 1)."""
     th = 2.0 * math.pi * (view % N_VIEWS) / N_VIEWS
     x, y, z = CAM_POS
-    pos = (x * math.cos(th) + z * math.sin(th), y, -x * math.sin(th) + z * math.cos(th))
-    return P.Camera(pos, (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, width, height)
+    return (x * math.cos(th) + z * math.sin(th), y, -x * math.sin(th) + z * math.cos(th))
 
 
-def load_peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    try:
-        with open(p) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+def workload_config(name: str, world: int, streams: int) -> dict:
+    """The bench line's `config`, identical in both arms (it depends on the arguments only)."""
+    if name == "cfg2":
+        objects = [f"{k}:{kw}" for k, kw in CFG2_OBJECTS]
+        rays = 800 * 800 * len(objects) * world
+        par = (f"weak: each of {world} GPU(s) samples its own orbit view of every object per step "
+               f"(views interleaved over ranks), objects over {streams} CUDA stream(s)")
+    else:
+        objects = {"cfg1": ["shell s1"], "cfg3": ["blobs s1 x4 cascade"], "cfg4": ["blobs s1 512^3"]}[name]
+        rays = {"cfg1": 800 * 800, "cfg3": 1297 * 840, "cfg4": 1 << 24}[name]
+        par = (f"strong: the step's rays split into {world} contiguous range(s) of ceil(N/{world}) "
+               f"(global ray_indices), ranges over {streams} CUDA stream(s)")
+    return {"workload": name, "desc": DESC[name], "variant": "sparse+hdda+skip", "rays_per_step": rays,
+            "objects": objects, "parallelism": par,
+            "l2": "inputs+outputs per step > 126 MB L2 (no flush)"}
 
 
-class ClockSampler:
-    """SM clocks + throttle reasons sampled through NVML every 5 ms while the timed region runs
-    (nvidia-smi's own polling starts too slowly for a sub-second region); falls back to
-    `nvidia-smi -lms` when NVML is unavailable."""
-
-    # nvmlClocksEventReasons bits (nvml.h)
-    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
-            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
-
-    def __init__(self, index: int):
-        self.index, self.rows, self.stop = index, [], threading.Event()
-        self.max_mhz = None
-
-    def __enter__(self):
-        try:
-            import pynvml as N
-            N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
-            get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                N.nvmlDeviceGetCurrentClocksThrottleReasons
-
-            def poll():
-                while not self.stop.is_set():
-                    try:
-                        self.rows.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), int(get_r(h))))
-                    except Exception:
-                        pass
-                    time.sleep(0.005)
-            self.t = threading.Thread(target=poll, daemon=True)
-            self.t.start()
-        except Exception:
-            self.t = None
-        return self
-
-    def __exit__(self, *a):
-        self.stop.set()
-        if self.t is not None:
-            self.t.join(timeout=1)
-
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
-        sm = [r[0] for r in self.rows]
-        reasons = sorted({name for _, m in self.rows for b, name in self.BITS.items() if m & b})
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml"}
+def scaling_of(name: str) -> str:
+    return "weak" if name == "cfg2" else "strong"
 
 
-# ---------------------------------------------------------------------------
-# workloads
-# ---------------------------------------------------------------------------
+class ProductGen:
+    """Input generation through the package's host generators (libsogk.so; pinned to the
+    reference generators by tests/test_host.py) -- the GPU arm."""
+
+    def __init__(self, P):
+        self.P = P
+
+    def scene(self, kind, res, seed=1, count=12, fraction=0.05):
+        t = self.P.GridTransform.cube(res, (-1.0, -1.0, -1.0), 2.0)
+        bits, occ = self.P.generate_scene(kind, t, seed=seed, count=count, fraction=fraction)
+        return [(t.resolution, t.world_min, t.voxel_size, bits)], occ
+
+    def cascade(self, kind, res, levels, seed=1):
+        base = self.P.GridTransform.cube(res, (-1.0, -1.0, -1.0), 2.0)
+        return [(t.resolution, t.world_min, t.voxel_size, b)
+                for t, b in self.P.build_dense_cascade(kind, base, levels, seed=seed)]
+
+    def camera_rays(self, pos, w, h, first, count):
+        return self.P.Camera(pos, (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, w, h).rays(first, count)
+
+    def probe_rays(self, level, n, seed):
+        return self.P.make_probe_rays(self.P.GridTransform(*level[:3]), n, seed)
+
+
+class RefGen:
+    """Input generation through the UNMODIFIED reference generators (oracle/_ref/libsogref.so:
+    scene_gen.hpp, camera.hpp, bench.hpp make_probe_rays) -- the reference arm, which must not
+    load the product library."""
+
+    def __init__(self):
+        from oracle_bindings import RefLib
+
+        self.R = RefLib()
+
+    def scene(self, kind, res, seed=1, count=12, fraction=0.05):
+        g = self.R.scene(kind, res, seed=seed, fraction=fraction, count=count)
+        return [(g.res, g.wmin, g.voxel, g.bits)], float(np.unpackbits(g.bits).sum()) / float(res ** 3)
+
+    def cascade(self, kind, res, levels, seed=1):
+        return [(g.res, g.wmin, g.voxel, g.bits) for g in self.R.cascade(kind, levels, res, seed=seed)]
+
+    def camera_rays(self, pos, w, h, first, count):
+        return self.R.camera_rays(pos, (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, w, h)[first:first + count]
+
+    def probe_rays(self, level, n, seed):
+        from oracle_bindings import Grid
+
+        return self.R.probe_rays(Grid(level[0], level[1], level[2], level[3]), n, seed)
+
+
 class Workload:
-    """Grids (per object) + a ray generator per (step, object) + the schedule."""
+    """Grids (per object, as (resolution, world_min, voxel, bits) levels), the schedule, and
+    the rays of every (step, object, rank) -- the same inputs in both arms."""
 
-    def __init__(self, P, name: str):
-        self.P, self.name = P, name
+    def __init__(self, name: str, gen):
+        self.name, self.gen = name, gen
         self.ray_order = 0
-        base = P.GridTransform.cube(128, (-1.0, -1.0, -1.0), 2.0)
         self.cascade = False
-        self.schedule = P.StepSchedule.constant(0.5 * base.voxel_size)
+        vox128 = 2.0 / 128
+        self.schedule = (0, 0.5 * vox128, 0.0)  # (kind, dt0, growth)
+        self.width = self.height = 800
+        self.n_probe = 0
         if name == "cfg2":
             self.objects = []
             for kind, kw in CFG2_OBJECTS:
-                bits, occ = P.generate_scene(kind, base, **kw)
-                self.objects.append(dict(label=f"{kind}:{kw}", levels=[(base, bits)], occupancy=occ,
-                                         scene=(kind, kw.get("seed", 1), kw.get("count", 12), base)))
-            self.width = self.height = 800
-            self.desc = ("8 procedural 128^3 objects (shell s1, shell s2 n256, blobs s1..s4 n6..48, "
-                         "sponge s1, random 2%), 800x800 orbit views, dt0 = half voxel")
+                lv, occ = gen.scene(kind, 128, **kw)
+                self.objects.append(dict(label=f"{kind}:{kw}", levels=lv, occupancy=occ,
+                                         scene=(kind, kw.get("seed", 1), kw.get("count", 12))))
         elif name == "cfg1":
-            bits, occ = P.generate_scene("shell", base, seed=1)
-            self.objects = [dict(label="shell s1", levels=[(base, bits)], occupancy=occ,
-                                 scene=("shell", 1, 12, base))]
-            self.width = self.height = 800
-            self.desc = "single-level 128^3 shell s1, 800x800 bench camera, dt0 = half voxel"
+            lv, occ = gen.scene("shell", 128, seed=1)
+            self.objects = [dict(label="shell s1", levels=lv, occupancy=occ, scene=("shell", 1, 12))]
         elif name == "cfg3":
-            lv = P.build_dense_cascade("blobs", base, 4, seed=1)
-            self.objects = [dict(label="blobs s1 x4 cascade", levels=lv, occupancy=None,
-                                 scene=("blobs", 1, 12, base))]
+            lv = gen.cascade("blobs", 128, 4, seed=1)
+            self.objects = [dict(label="blobs s1 x4 cascade", levels=lv, occupancy=None, scene=("blobs", 1, 12))]
             self.cascade = True
             self.width, self.height = 1297, 840
-            self.schedule = P.StepSchedule.linear(0.5 * base.voxel_size, 1.0 / 256.0)
-            self.desc = "4-level 128^3 blobs s1 cascade, 1297x840 bench camera, linear dt0=2^-7 growth 1/256"
+            self.schedule = (1, 0.5 * vox128, 1.0 / 256.0)
         elif name == "cfg4":
-            t512 = P.GridTransform.cube(512, (-1.0, -1.0, -1.0), 2.0)
-            bits, occ = P.generate_scene("blobs", t512, seed=1)
-            self.objects = [dict(label="blobs s1 512^3", levels=[(t512, bits)], occupancy=occ)]
-            self.schedule = P.StepSchedule.constant(0.5 * t512.voxel_size)
+            lv, occ = gen.scene("blobs", 512, seed=1)
+            self.objects = [dict(label="blobs s1 512^3", levels=lv, occupancy=occ, scene=None)]
+            self.schedule = (0, 0.5 * 2.0 / 512, 0.0)
             self.n_probe = 1 << 24
             self.ray_order = 1  # incoherent probe rays: pass 1 bins them (sogk_sampler_set_ray_order)
-            self.desc = ("512^3 blobs s1 (1.44%), 2^24 make_probe_rays, dt0 = half voxel; pass 1 "
-                         "processes the rays binned by grid entry cell and direction")
         else:
             raise SystemExit(f"unknown config {name}")
+        self.desc = DESC[name]
+        self._probe_cache = {}
 
-    def camera(self, step_index: int, obj: int, rank: int, world: int):
-        """The camera of (global step, object) for this rank (None for probe-ray configs)."""
-        if self.name == "cfg4":
-            return None
-        view = view_of(step_index, rank, world, N_VIEWS, obj * (N_VIEWS // max(1, len(self.objects))))
-        if self.name in ("cfg1", "cfg3"):
-            view = 0
-        return orbit_camera(self.P, view, self.width, self.height)
-
-    def rays_per_object(self) -> int:
+    def frame_rays(self) -> int:
+        """Rays of one object per step before sharding."""
         return self.n_probe if self.name == "cfg4" else self.width * self.height
 
-    def fill_rays(self, out, step_index: int, obj: int, rank: int, world: int):
-        """Write the rays of (global step, object) for this rank into the CUDA tensor `out`."""
-        P = self.P
+    def shard(self, step: int, obj: int, rank: int, world: int) -> dict:
+        """The rays of (global step, object) for this rank: cfg2 -> one whole orbit view per rank
+        (weak scaling); cfg1/3/4 -> a contiguous ceil(N/G) range of the step's rays (SURVEY
+        §8e), ray_indices global (first = the range start)."""
+        if self.name == "cfg2":
+            view = view_of(step, rank, world, N_VIEWS, obj * (N_VIEWS // len(self.objects)))
+            return dict(kind="camera", pos=orbit_pos(view), first=0, count=self.width * self.height)
+        a, b = shard_range(self.frame_rays(), world, rank)
         if self.name == "cfg4":
+            return dict(kind="probe", seed=1000 + step, first=a, count=b - a)
+        return dict(kind="camera", pos=orbit_pos(0), first=a, count=b - a)
+
+    def rays_per_object(self, world: int = 1, rank: int = 0) -> int:
+        return self.shard(0, 0, rank, world)["count"]
+
+    def host_rays(self, spec: dict) -> np.ndarray:
+        if spec["kind"] == "camera":
+            return self.gen.camera_rays(spec["pos"], self.width, self.height, spec["first"], spec["count"])
+        key = spec["seed"]
+        if key not in self._probe_cache:
+            if len(self._probe_cache) > 2:
+                self._probe_cache.clear()
+            self._probe_cache[key] = self.gen.probe_rays(self.objects[0]["levels"][-1], self.n_probe, key)
+        return self._probe_cache[key][spec["first"]:spec["first"] + spec["count"]]
+
+    def fill_rays(self, P, out, spec: dict):
+        """GPU arm: the rays of `spec` into the CUDA tensor `out` (camera rays by the raygen
+        kernel, bit-identical to the host generator)."""
+        if spec["kind"] == "camera":
+            cam = P.Camera(spec["pos"], (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, self.width, self.height)
+            cam.rays_device(spec["first"], spec["count"], out=out)
+        else:
             import torch
 
-            t = self.objects[0]["levels"][0][0]
-            h = P.make_probe_rays(t, self.n_probe, seed=1000 + step_index * world + rank)
-            out.copy_(torch.from_numpy(h))
-            return
-        view = view_of(step_index, rank, world, N_VIEWS, obj * (N_VIEWS // max(1, len(self.objects))))
-        if self.name in ("cfg1", "cfg3"):
-            view = 0  # the bench camera pose of the config
-        cam = orbit_camera(P, view, self.width, self.height)
-        cam.rays_device(0, self.width * self.height, out=out)
+            out.copy_(torch.from_numpy(np.ascontiguousarray(self.host_rays(spec))))
 
-    def host_rays(self, step_index: int, obj: int, rank: int, world: int) -> np.ndarray:
-        P = self.P
-        if self.name == "cfg4":
-            t = self.objects[0]["levels"][0][0]
-            return P.make_probe_rays(t, self.n_probe, seed=1000 + step_index * world + rank)
-        view = view_of(step_index, rank, world, N_VIEWS, obj * (N_VIEWS // max(1, len(self.objects))))
-        if self.name in ("cfg1", "cfg3"):
-            view = 0  # the bench camera pose of the config
-        return orbit_camera(P, view, self.width, self.height).rays()
-
-
-def grid_bytes(P, levels_bits, analyzer):
-    if analyzer == P.Analyzer.dda:
-        return sum(int(b.size) for _, b in levels_bits)
-    return None  # filled from the VDB info
+    def camera(self, P, spec: dict):
+        return P.Camera(spec["pos"], (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, self.width, self.height)
 
 
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+VARIANT_NAMES = {"hdda_skip": "sparse+hdda+skip", "dda_branch": "dense+dda+branch",
+                 "dda_skip": "dense+dda+skip", "cd_skip": "dense+cd+skip"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -221,13 +250,18 @@ def run_gpu(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; ranks beyond the visible devices share them (tests: 2 ranks on 1 GPU)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
 
-    wl = Workload(P, args.config)
+    wl = Workload(args.config, ProductGen(P))
+    sched = P.StepSchedule(*wl.schedule)
     n_obj = len(wl.objects)
     # --- grids: rank 0's payloads broadcast once over NVLink (NCCL), VDB built per rank (K1)
     grids = []
@@ -236,7 +270,8 @@ def run_gpu(args):
     dist_grids = []
     for o in wl.objects:
         dense_lv, vdb_lv, cd_lv = [], [], []
-        for t, bits in o["levels"]:
+        for res, wmin, voxel, bits in o["levels"]:
+            t = P.GridTransform(res, wmin, voxel)
             d_bits = torch.from_numpy(bits).to(dev)
             broadcast_payload(d_bits)  # once, NCCL over NVLink; rank 0's payload wins
             dg = P.DenseGrid(t, d_bits)
@@ -258,7 +293,7 @@ def run_gpu(args):
         grids.append((dense_lv, vdb_lv))
         dist_grids.append(cd_lv)
     vdb_bytes = [sum(int(v.memory_bytes()) for v in vl) for _, vl in grids]
-    dense_bytes = [sum(int(t.payload_bytes()) for t, _ in o["levels"]) for o in wl.objects]
+    dense_bytes = [sum(int(b.size) for *_, b in o["levels"]) for o in wl.objects]
 
     variants = {
         "hdda_skip": (P.Analyzer.hdda, P.KernelKind.skip),
@@ -272,18 +307,20 @@ def run_gpu(args):
     for vname, (an, kk) in variants.items():
         samplers[vname] = [P.Sampler(grids[i][1] if an == P.Analyzer.hdda else
                                      dist_grids[i] if an == P.Analyzer.cd else grids[i][0], an, kk,
-                                     wl.schedule, cascade=wl.cascade, ray_order=wl.ray_order)
+                                     sched, cascade=wl.cascade, ray_order=wl.ray_order)
                            for i in range(n_obj)]
 
-    nr = wl.rays_per_object()
     steps_total = args.warmup + args.steps
+    specs = [[wl.shard(s, o, rank, world) for o in range(n_obj)] for s in range(steps_total)]
+    nr = specs[0][0]["count"]  # this rank's rays per object per step
     # --- rays for every (step, object) in HBM before timing
     rays = [[torch.empty((nr, 8), dtype=torch.float64, device=dev) for _ in range(n_obj)]
             for _ in range(steps_total)]
     for s in range(steps_total):
         for o in range(n_obj):
-            wl.fill_rays(rays[s][o], s, o, rank, world)
+            wl.fill_rays(P, rays[s][o], specs[s][o])
     torch.cuda.synchronize()
+    base0 = specs[0][0]["first"]  # global index of this rank's first ray (same every step)
 
     # parts: the units one count/write pair processes -- one per object, or, for single-object
     # configs on several streams, one contiguous ray range per stream (each its own packed batch)
@@ -326,16 +363,10 @@ def run_gpu(args):
                 per[o] += totals[(vname, s, pi)]
             for o in range(n_obj):
                 obj_cap[o] = max(obj_cap[o], per[o])
-    # hit rays per (step, part) for the write kernel's algorithmic bytes
-    hits = {}
-    for s in range(steps_total):
-        for pi, (o, a, b) in enumerate(parts):
-            smp = samplers[next(iter(samplers))][o]
-            smp.count(prays(s, pi), packed_info=packed[pi], stats=stats[pi])
-            hits[(s, pi)] = int((packed[pi][:, 1] > 0).sum().item())
 
     stream = torch.cuda.current_stream()
     results = {}
+    launches_per_step = {}
     for vname, smp in samplers.items():
         def one_step(s, ev=None):
             for pi, (o, a, b) in enumerate(parts):
@@ -344,7 +375,7 @@ def run_gpu(args):
                 smp[o].count(prays(s, pi), packed_info=packed[pi], stats=stats[pi])
                 if ev is not None:
                     ev[pi][1].record(stream)
-                smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=a,
+                smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=base0 + a,
                              out=outs[pi], cells=True, levels=False)
                 if ev is not None:
                     ev[pi][2].record(stream)
@@ -378,7 +409,7 @@ def run_gpu(args):
                 for pi, (o, a, b) in enumerate(parts):
                     st = side[pi % args.streams]
                     smp[o].count(prays(s, pi), packed_info=packed[pi], stats=stats[pi], stream=st)
-                    smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=a,
+                    smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=base0 + a,
                                  out=outs[pi], cells=True, levels=False, stream=st)
 
             for st in side:
@@ -408,29 +439,71 @@ def run_gpu(args):
         count_ms = sum(evs[k][pi][0].elapsed_time(evs[k][pi][1]) for k in range(args.steps) for pi in range(n_parts))
         write_ms = sum(evs[k][pi][1].elapsed_time(evs[k][pi][2]) for k in range(args.steps) for pi in range(n_parts))
         samples = sum(totals[(vname, args.warmup + k, pi)] for k in range(args.steps) for pi in range(n_parts))
-        nhit = sum(hits[(args.warmup + k, pi)] for k in range(args.steps) for pi in range(n_parts))
         results[vname] = dict(ms=ms, ms_serial=ms_serial, count_ms=count_ms, write_ms=write_ms, samples=samples,
-                              hit_rays=nhit, clocks=clk.summary())
+                              clocks=clk.summary())
+        # our kernels per count/write pair: count + scan (+ bin_count, scan, bin_scatter when the
+        # rays are binned) and gather + tail
+        launches_per_step[vname] = n_parts * (4 + (3 if wl.ray_order else 0))
+
+    # --- parity of what was timed: the first timed step of every variant, re-run untimed
+    # (same inputs, same kernels) and kept for the reference check in the cpu_baseline leg
+    keep = {}
+    if world == 1 and not args.no_cpu_baseline:
+        s_chk = args.warmup
+        for vname, smp in samplers.items():
+            per_obj = []
+            for o in range(n_obj):
+                d = rays[s_chk][o]
+                out = smp[o].sample(d, ray_index_base=base0, with_counters=False)
+                stride = args.parity_stride
+                idx = torch.arange(0, nr, stride, device=dev)
+                pk = out.packed_info[idx]
+                cnt = pk[:, 1]
+                if int(cnt.sum().item()) > 0:
+                    rep = torch.repeat_interleave(pk[:, 0], cnt)
+                    off = torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt)
+                    g = rep + (torch.arange(int(cnt.sum().item()), device=dev) - off)
+                else:
+                    g = torch.zeros(0, dtype=torch.int64, device=dev)
+                per_obj.append(dict(
+                    counts=cnt.cpu().numpy(), status=out.status[idx].cpu().numpy(),
+                    t_starts=out.t_starts[g].cpu().numpy(), t_ends=out.t_ends[g].cpu().numpy(),
+                    ray_indices=out.ray_indices[g].cpu().numpy(),
+                    cells=out.cells[g].cpu().numpy().view(np.uint32)))
+                del out
+            keep[vname] = per_obj
+        torch.cuda.synchronize()
+
+    if args.dump:  # every rank's outputs of the first timed step (tests: rank-count invariance)
+        os.makedirs(args.dump, exist_ok=True)
+        smp = samplers[next(iter(samplers))]
+        for o in range(n_obj):
+            out = smp[o].sample(rays[args.warmup][o], ray_index_base=base0)
+            np.savez(os.path.join(args.dump, f"rank{rank}_obj{o}.npz"), first=base0,
+                     packed_info=out.packed_info.cpu().numpy(), t_starts=out.t_starts.cpu().numpy(),
+                     t_ends=out.t_ends.cpu().numpy(), ray_indices=out.ray_indices.cpu().numpy(),
+                     cells=out.cells.cpu().numpy(), status=out.status.cpu().numpy())
+        torch.cuda.synchronize()
 
     P.release_workspaces()
-    # --- render leg: render_frame fused (sample + composite per pixel, no sample arrays),
-    # the paper's rendered-frames metric; one frame = one object's view
+    # --- render leg: render_frame (pass 1 + pass 2 on the camera rays, shading + compositing),
+    # the paper's rendered-frames metric; one frame = one object's view (this rank's pixels)
     render = None
     if not args.no_render and wl.name != "cfg4":
-        scenes = [P.analytic_scene(o["scene"][0], o["scene"][3], seed=o["scene"][1], count=o["scene"][2])
-                  for o in wl.objects]
-        npx = wl.width * wl.height
-        r_res = torch.empty((npx, 5), dtype=torch.float64, device=dev)
-        r_rgb = torch.empty((npx, 3), dtype=torch.uint8, device=dev)
+        scenes = [P.analytic_scene(o["scene"][0], P.GridTransform(*o["levels"][0][:3]), seed=o["scene"][1],
+                                   count=o["scene"][2]) for o in wl.objects]
+        r_res = torch.empty((nr, 5), dtype=torch.float64, device=dev)
+        r_rgb = torch.empty((nr, 3), dtype=torch.uint8, device=dev)
         r_st = torch.zeros(8, dtype=torch.int64, device=dev)
         render = {}
         for vname, smp in samplers.items():
             def rstep(s_):
                 for o in range(n_obj):
-                    cam = wl.camera(s_, o, rank, world)._c()
-                    P._check(P.lib.sogk_render_camera(smp[o]._h, scenes[o].handle, P.C.byref(cam), 0, npx,
-                                                      r_res.data_ptr(), r_rgb.data_ptr(), r_st.data_ptr(),
-                                                      stream.cuda_stream or None), "render")
+                    sp = specs[s_][o]
+                    cam = wl.camera(P, sp)._c()
+                    P._check(P.lib.sogk_render_camera(smp[o]._h, scenes[o].handle, P.C.byref(cam), sp["first"],
+                                                      sp["count"], r_res.data_ptr(), r_rgb.data_ptr(),
+                                                      r_st.data_ptr(), stream.cuda_stream or None), "render")
             for s_ in range(args.warmup):
                 rstep(s_)
             if world > 1:
@@ -445,7 +518,7 @@ def run_gpu(args):
             rms = e0.elapsed_time(e1)
             frames = args.steps * n_obj
             render[vname] = {"frames_per_sec": frames / (rms / 1e3), "ms_per_frame": rms / frames,
-                             "mpix_per_sec": frames * npx / (rms / 1e3) / 1e6}
+                             "mpix_per_sec": frames * nr / (rms / 1e3) / 1e6}
 
     # --- e2e through the host C-ABI entry point (pinned host buffers, H2D/D2H timed)
     e2e = None
@@ -469,7 +542,6 @@ def run_gpu(args):
                      t_starts=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
                      t_ends=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
                      ray_indices=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy(),
-                     cells=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
                      stats=np.zeros(8, np.int64))
             o["counters"] = torch.empty((nr, 3), dtype=torch.int32, pin_memory=True).numpy()
             return o
@@ -479,18 +551,18 @@ def run_gpu(args):
         pool = ThreadPoolExecutor(n_workers) if n_workers > 1 else None
 
         def e2e_objects(s, full, w):
-            # full: the packed intervals (t_starts, t_ends, ray_indices, cells); otherwise what
-            # the reference's run_sampler returns per ray (sampling.hpp:157-164): its sample
-            # buffer (packed t_starts + packed_info) and its three counters.  Worker w takes the
-            # objects o = w mod n_workers (independent samplers: each call is synchronous and
-            # pipelines its own chunks; ctypes drops the GIL, so the calls overlap)
+            # full: the north-star packed intervals (packed_info, t_starts, t_ends, ray_indices);
+            # lean: what the reference's run_sampler returns per ray (sampling.hpp:157-164), its
+            # sample buffer (packed t_starts + packed_info) and its three counters.  Worker w
+            # takes the objects o = w mod n_workers (independent samplers: each call is
+            # synchronous and pipelines its own chunks; ctypes drops the GIL, so calls overlap)
             h_out = h_outs[w]
             for o in range(w, n_obj, n_workers):
-                rc = lib.sogk_sample_host(smp[o]._h, h_rays[s][o].data_ptr(), nr, 0, hcap,
+                rc = lib.sogk_sample_host(smp[o]._h, h_rays[s][o].data_ptr(), nr, base0, hcap,
                                           h_out["packed_info"].ctypes.data, h_out["t_starts"].ctypes.data,
                                           h_out["t_ends"].ctypes.data if full else None,
                                           h_out["ray_indices"].ctypes.data if full else None,
-                                          h_out["cells"].ctypes.data if full else None, None, None,
+                                          None, None, None,
                                           None if full else h_out["counters"].ctypes.data,
                                           h_out["stats"].ctypes.data, stream.cuda_stream or None)
                 P._check(rc, "sample_host")
@@ -519,14 +591,14 @@ def run_gpu(args):
                 sec = float(tt.item())
             return sec
 
-        e2e_s = timed(False)
         e2e_full_s = timed(True)
+        e2e_lean_s = timed(False)
         samples0 = sum(totals[(vname0, args.warmup + k, pi)] for k in range(args.steps) for pi in range(n_parts))
         if pool is not None:
             pool.shutdown()
-        e2e = dict(seconds=e2e_s, h2d=nr * 64 * n_obj, workers=n_workers,
-                   d2h_per_run=samples0 * 8 / args.steps + nr * (16 + 12) * n_obj,
-                   full_seconds=e2e_full_s, full_d2h=samples0 * 24 / args.steps + nr * 16 * n_obj)
+        e2e = dict(full_seconds=e2e_full_s, lean_seconds=e2e_lean_s, h2d=nr * 64 * n_obj, workers=n_workers,
+                   full_d2h=samples0 * 20 / args.steps + nr * 16 * n_obj,
+                   lean_d2h=samples0 * 8 / args.steps + nr * (16 + 12) * n_obj)
 
     # --- max over ranks
     def rmax(x):
@@ -546,9 +618,8 @@ def run_gpu(args):
     agg = {}
     for vname, r in results.items():
         agg[vname] = dict(ms=rmax(r["ms"]), ms_serial=rmax(r["ms_serial"]), samples=rsum(r["samples"]),
-                          count_ms=r["count_ms"],
-                          write_ms=r["write_ms"], hit_rays=r["hit_rays"], local_samples=r["samples"],
-                          clocks=r["clocks"])
+                          rays=rsum(nr * n_obj * args.steps), count_ms=r["count_ms"], write_ms=r["write_ms"],
+                          local_samples=r["samples"], clocks=r["clocks"])
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -556,7 +627,7 @@ def run_gpu(args):
 
     head = "hdda_skip" if "hdda_skip" in agg else next(iter(agg))
     h = agg[head]
-    total_rays = nr * n_obj * args.steps * world
+    total_rays = h["rays"]  # every rank's rays of the timed steps
     sec = h["ms"] / 1e3
     rays_s = total_rays / sec
     samples_s = h["samples"] / sec
@@ -564,8 +635,8 @@ def run_gpu(args):
     # roofline: dominant kernel (larger share of the step) with its algorithmic bytes
     # (SURVEY §8(d)): pass 1 reads the rays (64 B) and writes packed_info (16 B) per ray;
     # pass 2 reads packed_info (16 B/ray) and writes the samples (24 B each).  The slabs
-    # pass 1 hands to pass 2 (12 B/sample each way) are not algorithmic; ncu's DRAM bytes
-    # (`traffic`, profiles/traffic_<cfg>.json) show them.
+    # pass 1 hands to pass 2 are not algorithmic; ncu's DRAM bytes (`traffic`,
+    # profiles/traffic_<cfg>.json) show them.
     launches = args.steps * n_parts
     nr_loc = nr * n_obj * args.steps
     write_bytes = nr_loc * 16 + h["local_samples"] * 24
@@ -617,7 +688,7 @@ def run_gpu(args):
             issue = {"error": str(e)}
 
     line = {
-        "metric": "rays/sec and samples/sec per B200 (and 8-GPU box), HDDA-VDB vs dense-DDA, % HBM roofline",
+        "metric": METRIC,
         "value": rays_s,
         "unit": "rays/s",
         "n_gpus": world,
@@ -625,134 +696,175 @@ def run_gpu(args):
         "warmup": args.warmup,
         "ms_per_step": h["ms"] / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling_of(args.config),
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (procedural occupancy grids from the reference generators, camera/probe rays)",
-        "config": {"workload": args.config, "desc": wl.desc, "variant": "sparse+hdda+skip" if head == "hdda_skip" else head,
-                   "rays_per_step": nr * n_obj * world, "objects": [o["label"] for o in wl.objects],
-                   "parallelism": f"rays sharded by view over {world} GPU(s), objects over {args.streams} stream(s)",
-                   "l2": "inputs+outputs per step > 126 MB L2 (no flush)"},
+        "config": workload_config(args.config, world, args.streams),
         "samples_per_sec": samples_s,
         "samples_per_step": h["samples"] / args.steps,
-        "variants": {k: {"rays_per_sec": total_rays / (v["ms"] / 1e3),
+        "gpu_launches": launches_per_step[head] * args.steps,
+        "clocks": h["clocks"],
+    }
+    if e2e:
+        line["e2e"] = {"value": total_rays / e2e["full_seconds"], "unit": "rays/s",
+                       "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["full_d2h"]),
+                       "api": "sogk_sample_host: pinned host rays in; out the north-star packed intervals "
+                              "(packed_info, t_starts, t_ends, ray_indices)",
+                       "host_threads": e2e["workers"],
+                       "lean": {"value": total_rays / e2e["lean_seconds"], "unit": "rays/s",
+                                "d2h_bytes_per_step": int(e2e["lean_d2h"]),
+                                "outputs": "what run_sampler returns per ray (sampling.hpp:157-164): "
+                                           "packed t_starts + packed_info + the three counters"}}
+    line["roofline"] = {
+        "bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": traffic.get(dom_key, {}).get("dram_bytes_per_launch"),
+        "peak_source": peak_src, "algorithmic_bytes_per_launch": dom["bytes"] / launches,
+        "note": "pass 1 is bound by traversal issue/latency, not HBM (DESIGN.md §4); traffic = ncu "
+                "dram read+write of one launch (object 0), " + traffic.get("source", "no capture committed"),
+        "other_pass": {"kernel": other["kernel"], "achieved": gbs(other), "frac": gbs(other) / peak,
+                       "algorithmic_bytes_per_launch": other["bytes"] / launches,
+                       "traffic": traffic.get(other_key, {}).get("dram_bytes_per_launch")},
+        "issue_ceiling": issue}
+    if world == 1 and not args.no_cpu_baseline:
+        cb, parity = cpu_baseline_and_parity(wl, args, keep, base0)
+        line["cpu_baseline"] = cb
+        line["parity"] = parity
+    line.update({
+        "variants": {k: {"rays_per_sec": v["rays"] / (v["ms"] / 1e3),
                          "samples_per_sec": v["samples"] / (v["ms"] / 1e3),
                          "ms_per_step": v["ms"] / args.steps,
                          "ms_per_step_one_stream": v["ms_serial"] / args.steps,
                          "count_ms_per_step": v["count_ms"] / args.steps,
                          "write_ms_per_step": v["write_ms"] / args.steps} for k, v in agg.items()},
         "hdda_vs_dda_branch": (agg["dda_branch"]["ms"] / agg["hdda_skip"]["ms"]) if {"dda_branch", "hdda_skip"} <= agg.keys() else None,
-        "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic.get(dom_key, {}).get("dram_bytes_per_launch"),
-                     "peak_source": peak_src, "algorithmic_bytes_per_launch": dom["bytes"] / launches,
-                     "note": "pass 1 is bound by traversal issue/latency and L1/L2 store transactions, "
-                             "not HBM (DESIGN.md §4); traffic = ncu dram read+write of one launch "
-                             "(object 0), " + traffic.get("source", "no capture committed"),
-                     "other_pass": {"kernel": other["kernel"], "achieved": gbs(other), "frac": gbs(other) / peak,
-                                    "algorithmic_bytes_per_launch": other["bytes"] / launches,
-                                    "traffic": traffic.get(other_key, {}).get("dram_bytes_per_launch")},
-                     "issue_ceiling": issue},
         "step_roofline": {"bytes_per_step": step_bytes / args.steps, "achieved_gbs": step_gbs,
                           "frac": step_gbs / peak,
                           "basis": "N_rays*(64+16) + N_samples*24 + VDB bytes (SURVEY §8d)"},
         "vdb_build_ms": build_ms,
         "distance_build_ms": dist_ms,
         "grid_bytes": {"dense": dense_bytes, "vdb_sog1": vdb_bytes},
-        "render": ({"what": "render_frame fused on the GPU (Camera::pixel_ray -> sampling -> "
-                             "composite_detailed -> Image::set_pixel per pixel, no sample arrays), "
-                             f"{wl.width}x{wl.height} frames, rank 0",
-                     "variants": render} if render else None),
-        "gpu_launches": 4 * launches,  # count, scan, gather, tail per object
-        "clocks": h["clocks"],
-    }
-    if e2e:
-        line["e2e"] = {"value": total_rays / e2e["seconds"], "unit": "rays/s",
-                       "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["d2h_per_run"]),
-                       "api": "sogk_sample_host: pinned host rays in; out, what run_sampler returns per ray "
-                              "(sampling.hpp:157-164): its samples (packed t_starts + packed_info) and "
-                              "its three counters",
-                       "host_threads": e2e["workers"],
-                       "full_intervals": {"value": total_rays / e2e["full_seconds"], "unit": "rays/s",
-                                          "d2h_bytes_per_step": int(e2e["full_d2h"]),
-                                          "outputs": "packed_info, t_starts, t_ends, ray_indices, cells"}}
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(P, wl, args)
+        "render": ({"what": "render_frame on the GPU (pass 1 + pass 2 on the camera rays, per-sample "
+                            "shading, per-ray composite_detailed + Image::set_pixel), "
+                            f"{wl.width}x{wl.height} frames ({nr} pixels per rank), rank 0",
+                    "variants": render} if render else None),
+    })
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle/_ref: the unmodified reference headers) — baseline only
+# CPU reference (oracle/_ref: the unmodified reference headers) -- the cpu_baseline leg and the
+# reference arm; the only places bench.py loads anything under oracle/
 # ---------------------------------------------------------------------------
-def _ref_sampler(wl, analyzer, kernel):
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_bindings import Grid, RefLib
+def _ref_levels(o):
+    from oracle_bindings import Grid
+
+    return [Grid(tuple(r), tuple(w), v, b) for r, w, v, b in o["levels"]]
+
+
+def _ref_samplers(wl, analyzer, kernel):
+    from oracle_bindings import RefLib
 
     R = RefLib()
-    out = []
-    for o in wl.objects:
-        lv = [Grid(t.resolution, t.world_min, t.voxel_size, b) for t, b in o["levels"]]
-        out.append(R.sampler(lv, analyzer, kernel, wl.schedule.kind, wl.schedule.dt0,
-                             wl.schedule.growth, cascade=wl.cascade))
-    return R, out
+    k, dt0, gr = wl.schedule
+    return R, [R.sampler(_ref_levels(o), analyzer, kernel, k, dt0, gr, cascade=wl.cascade) for o in wl.objects]
 
 
-def _cpu_sample(wl, stride, step_index, rank=0, world=1):
-    return [wl.host_rays(step_index, o, rank, world)[::stride].copy() for o in range(len(wl.objects))]
-
-
-def _spin_mask(wl, rays_per_obj):
+def _spin_masks(wl, rays_per_obj):
     """Rays on which the reference HDDA never returns are screened out with the
     capped oracle detector; they are excluded from the CPU timing and counted."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_bindings import HDDA, SKIP, Grid, Oracle
+    from oracle_bindings import HDDA, SKIP, Oracle
 
     O = Oracle()
+    k, dt0, gr = wl.schedule
     masks = []
     for o, r in zip(wl.objects, rays_per_obj):
-        lv = [Grid(t.resolution, t.world_min, t.voxel_size, b) for t, b in o["levels"]]
-        s = O.sampler(lv, HDDA, SKIP, wl.schedule.kind, wl.schedule.dt0, wl.schedule.growth,
-                      cascade=wl.cascade)
+        s = O.sampler(_ref_levels(o), HDDA, SKIP, k, dt0, gr, cascade=wl.cascade)
         masks.append((O.sample(s, r).status == 2).astype(np.uint8))
     return masks
 
 
-def cpu_baseline(P, wl, args):
-    from oracle_bindings import HDDA, SKIP
+def _strided_rays(wl, stride, step, rank=0, world=1):
+    return [np.ascontiguousarray(wl.host_rays(wl.shard(step, o, rank, world))[::stride])
+            for o in range(len(wl.objects))]
+
+
+def cpu_baseline_and_parity(wl, args, keep, base0):
+    """cpu_baseline: the unmodified reference sampler (oracle/_ref) timed on the host cores
+    over a strided sample of step 0's rays.  parity: the GPU outputs of the first timed step
+    (every variant bench timed) on a strided subset of its rays against the reference's
+    run_sampler on the same rays -- counts, t_starts, t_ends, ray_indices and cells bit for bit."""
+    from oracle_bindings import BRANCH, CD, DDA, HDDA, SKIP
 
     try:
-        R, smp = _ref_sampler(wl, HDDA, SKIP)
+        R, smp = _ref_samplers(wl, HDDA, SKIP)
     except FileNotFoundError:
-        return {"value": None, "unit": "rays/s", "kind": "reference", "cores": 0,
-                "sample": "oracle/_ref missing"}
+        return ({"value": None, "unit": "rays/s", "kind": "reference", "cores": 0,
+                 "sample": "oracle/_ref missing"}, {"status": "unchecked (oracle/_ref missing)"})
     cores = os.cpu_count() or 1
     stride = args.cpu_stride
-    rays = _cpu_sample(wl, stride, 0)
-    masks = _spin_mask(wl, rays)
+    rays = _strided_rays(wl, stride, 0)
+    masks = _spin_masks(wl, rays)
     sec, n = 0.0, 0
     for s, r, m in zip(smp, rays, masks):
         dt, _ = s.time(r, skip=m, threads=cores, reps=1)
         sec += dt
         n += int(r.shape[0] - m.sum())
-    return {"value": n / sec, "unit": "rays/s", "cores": cores, "kind": "reference",
-            "sample": f"sparse+hdda+skip via sog::run_sampler, every {stride}th ray of step 0 "
-                      f"({n} rays over {len(rays)} object(s)), {cores} threads, spin-screened "
-                      f"{int(sum(m.sum() for m in masks))} rays"}
+    cb = {"value": n / sec, "unit": "rays/s", "cores": cores, "kind": "reference",
+          "sample": f"sparse+hdda+skip via sog::run_sampler, every {stride}th ray of step 0 "
+                    f"({n} rays over {len(rays)} object(s)), {cores} threads, spin-screened "
+                    f"{int(sum(m.sum() for m in masks))} rays"}
+    # parity on the first timed step
+    an_k = {"hdda_skip": (HDDA, SKIP), "dda_branch": (DDA, BRANCH), "dda_skip": (DDA, SKIP), "cd_skip": (CD, SKIP)}
+    ps = args.parity_stride
+    prays = _strided_rays(wl, ps, args.warmup)
+    pmasks = _spin_masks(wl, prays)
+    checked, bad, rays_checked, samples_checked, screened = [], [], 0, 0, 0
+    for vname, per_obj in keep.items():
+        an, k = an_k[vname]
+        _, rs = _ref_samplers(wl, an, k)
+        for o, (s, r, m, got) in enumerate(zip(rs, prays, pmasks, per_obj)):
+            und = (got["status"] == 2).astype(np.uint8)
+            skip = np.maximum(m, und)
+            want = s.sample(r, skip=skip, threads=cores)
+            ok_rays = skip == 0
+            gc = np.where(ok_rays, got["counts"], 0)
+            wc = want.packed_info[:, 1]
+            sel = np.repeat(ok_rays, got["counts"])
+            ri_want = np.repeat(np.arange(r.shape[0], dtype=np.int64) * ps + base0, wc).astype(np.int32)
+            same = (np.array_equal(gc, wc)
+                    and np.array_equal(got["t_starts"][sel].view(np.uint64), want.t_starts.view(np.uint64))
+                    and np.array_equal(got["t_ends"][sel].view(np.uint64), want.t_ends.view(np.uint64))
+                    and np.array_equal(got["ray_indices"][sel], ri_want)
+                    and np.array_equal(got["cells"][sel], want.cells))
+            rays_checked += int(ok_rays.sum())
+            samples_checked += int(wc.sum())
+            screened += int(skip.sum())
+            (checked if same else bad).append(f"{VARIANT_NAMES[vname]}:{wl.objects[o]['label']}")
+    parity = {"status": "bit-exact" if not bad and checked else ("MISMATCH" if bad else "unchecked"),
+              "against": "oracle/_ref (the unmodified reference run_sampler / run_cascade_sampler)",
+              "step": args.warmup, "ray_stride": ps, "rays_checked": rays_checked,
+              "samples_checked": samples_checked, "spin_screened_rays": screened,
+              "outputs": "per-ray counts, t_starts, t_ends, ray_indices, cells (bit-exact)",
+              "cases_ok": len(checked), "cases_bad": bad}
+    return cb, parity
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU sampler (oracle/_ref) on the host cores."""
+    """--impl reference: the reference CPU sampler (oracle/_ref, the unmodified headers) on the
+    host cores, inputs generated by the reference's own generators; the product library is
+    never loaded in this process."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2404_10272_b200 as P
     from oracle_bindings import HDDA, SKIP
 
-    wl = Workload(P, args.config)
     try:
-        R, smp = _ref_sampler(wl, HDDA, SKIP)
+        wl = Workload(args.config, RefGen())
+        R, smp = _ref_samplers(wl, HDDA, SKIP)
     except FileNotFoundError as e:
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
         return
@@ -760,15 +872,20 @@ def run_reference(args):
     stride = args.cpu_stride
     step_rays, step_masks = [], []
     for s in range(args.warmup + args.steps):
-        r = _cpu_sample(wl, stride, s, 0, 1)
+        r, m = [], []
+        for rk in range(world):  # the whole job's rays of this step (every rank's share)
+            rr = _strided_rays(wl, stride, s, rk, world)
+            r += rr
+            m += _spin_masks(wl, rr)
         step_rays.append(r)
-        step_masks.append(_spin_mask(wl, r))
+        step_masks.append(m)
     per_step_rays = [sum(int(x.shape[0] - m.sum()) for x, m in zip(r, mm)) for r, mm in zip(step_rays, step_masks)]
+    n_obj = len(wl.objects)
 
     def step(s):
         t = 0.0
-        for sm, r, m in zip(smp, step_rays[s], step_masks[s]):
-            dt, _ = sm.time(r, skip=m, threads=cores, reps=1)
+        for i, (r, m) in enumerate(zip(step_rays[s], step_masks[s])):
+            dt, _ = smp[i % n_obj].time(r, skip=m, threads=cores, reps=1)
             t += dt
         return t
 
@@ -780,15 +897,17 @@ def run_reference(args):
         total_s += step(args.warmup + k)
         n += per_step_rays[args.warmup + k]
     v = n / total_s
+    sample = (f"every {stride}th ray of each step's rays (all ranks' shares), sog::run_sampler "
+              f"(sparse+hdda+skip) on {cores} threads, inputs from the reference generators, "
+              f"spin-screened {sum(int(m.sum()) for mm in step_masks for m in mm)} rays")
     line = {
-        "impl": "reference",
-        "metric": "rays/sec and samples/sec per B200 (and 8-GPU box), HDDA-VDB vs dense-DDA, % HBM roofline",
+        "impl": "reference", "metric": METRIC,
         "value": v, "unit": "rays/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_s / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "desc": wl.desc, "variant": "sparse+hdda+skip"},
-        "cpu_baseline": {"value": v, "unit": "rays/s", "cores": cores, "kind": "reference",
-                         "sample": f"every {stride}th ray of each step's views, sog::run_sampler on {cores} threads"},
+        "ms_per_step": total_s / args.steps * 1e3, "higher_is_better": True,
+        "scaling": scaling_of(args.config), "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (procedural occupancy grids from the reference generators, camera/probe rays)",
+        "config": workload_config(args.config, world, args.streams),
+        "cpu_baseline": {"value": v, "unit": "rays/s", "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -804,6 +923,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--variants", default="")
     ap.add_argument("--cpu-stride", type=int, default=8)
+    ap.add_argument("--parity-stride", type=int, default=64,
+                    help="every k-th ray of the first timed step is checked against the reference")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-workers", type=int, default=2,
                     help="host threads issuing sogk_sample_host calls for different objects concurrently")
@@ -811,13 +932,14 @@ def main():
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams the step's objects are spread over (1: one stream)")
+    ap.add_argument("--backend", default="nccl", help="torch.distributed backend under torchrun (tests: gloo)")
+    ap.add_argument("--dump", default="", help="directory: every rank saves its outputs of the first timed step")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = {"cfg1": 200, "cfg2": 50, "cfg3": 200, "cfg4": 10}[args.config]
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
         run_reference(args)
     else:
         run_gpu(args)

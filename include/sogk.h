@@ -10,6 +10,9 @@
  * interface it replaces.
  *
  * Conventions
+ *  - Limits: n < 2^32 rays per call; ray_indices are int32, so ray_index_base + n - 1 <=
+ *    INT32_MAX when they are written; cells pack 10 bits per axis, so cells are refused
+ *    for grids above 1024 voxels on an axis (SOGK_INVALID_ARG).
  *  - Every function returns an int status (sogk_status); no exceptions cross
  *    the boundary.  sogk_last_error() returns the thread-local message of the
  *    last failure.
@@ -17,7 +20,11 @@
  *    host buffers ("h_" prefix) are caller-owned host pointers (pinned memory
  *    recommended).  `stream` is a cudaStream_t (NULL = legacy default stream).
  *  - Grids are immutable after creation and may be shared by samplers, host
- *    threads and streams (mirrors the reference, README "Concurrency").
+ *    threads and streams (mirrors the reference, README "Concurrency").  Builds are
+ *    stream-ordered; every sampling launch first waits (cudaStreamWaitEvent) for the
+ *    builds of its levels, so a grid built on one stream can be sampled on any other.
+ *  - sogk_sample_host and the render calls lock the sampler: one sampler may be called from
+ *    several host threads (the reference's render_frame does this through make_sampler).
  *    A sampler owns scratch memory: use one sampler per concurrent stream.
  *  - Rays are the reference `sog::Ray` layout (ray.hpp:92-114): 8 doubles per
  *    ray {origin.xyz, direction.xyz, t_min, t_max}, i.e. a std::vector<sog::Ray>
@@ -194,6 +201,19 @@ int sogk_sample_write(sogk_sampler* s, const double* d_rays, int64_t n,
                       const int64_t* d_packed_info, int64_t ray_index_base, double* d_t_starts,
                       double* d_t_ends, int32_t* d_ray_indices, uint32_t* d_cells,
                       uint8_t* d_levels, void* stream);
+/* The same two passes with an explicit pass-1 -> pass-2 handshake: sogk_sample_count_ex
+ * returns a token naming its run slabs, and sogk_sample_write_ex uses them only when it
+ * presents that token on the same stream (and sampler) with no other count in between;
+ * any other token (0 included) takes the exact cold path.  Use these when ray buffers are
+ * rewritten in place or counts run on several streams: the token-less calls match a write
+ * to its count by (sampler, stream, ray and packed_info pointers, n). */
+int sogk_sample_count_ex(sogk_sampler* s, const double* d_rays, int64_t n, int64_t* d_packed_info,
+                         int64_t* d_stats, uint8_t* d_status, int32_t* d_counters, void* stream,
+                         uint64_t* token);
+int sogk_sample_write_ex(sogk_sampler* s, const double* d_rays, int64_t n,
+                         const int64_t* d_packed_info, uint64_t token, int64_t ray_index_base,
+                         double* d_t_starts, double* d_t_ends, int32_t* d_ray_indices,
+                         uint32_t* d_cells, uint8_t* d_levels, void* stream);
 /* Camera-fused variants: the rays of pixels [first_pixel, first_pixel + n) are generated
  * in registers (Camera::pixel_ray, camera.hpp:167-179) instead of read from HBM. */
 int sogk_sample_count_camera(sogk_sampler* s, const sogk_camera* cam, int64_t first_pixel,

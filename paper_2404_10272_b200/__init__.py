@@ -120,6 +120,8 @@ _SIGS = {
     "sogk_release_workspaces": (C.c_int, []),
     "sogk_sample_count": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_write": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "sogk_sample_count_ex": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, C.POINTER(_u64)]),
+    "sogk_sample_write_ex": (C.c_int, [_vp, _vp, _i64, _vp, _u64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_count_camera": (C.c_int, [_vp, C.POINTER(_Camera), _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_write_camera": (C.c_int, [_vp, C.POINTER(_Camera), _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_host": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -476,6 +478,14 @@ class SampleRun:
         return self.analyzer_lookups + self.kernel_lookups
 
 
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
 def _torch():
     import torch
 
@@ -503,6 +513,7 @@ class Sampler:
         h = C.c_void_p()
         _check(lib.sogk_sampler_create(arr, len(levels), C.byref(d), C.byref(h)), "sampler")
         self._h = h.value
+        self._tokens = {}
         if ray_order:  # pass 1 in binned order (incoherent rays); outputs unchanged
             _check(lib.sogk_sampler_set_ray_order(self._h, ray_order), "ray order")
 
@@ -515,14 +526,22 @@ class Sampler:
             pass
 
     # -- device two-pass API ------------------------------------------------
+    # count() keeps the handshake token of its run slabs per packed_info buffer
+    # (sogk_sample_count_ex); write() presents the token of the count that last filled its
+    # packed_info, and the library uses the slabs only if that count is still the latest on the
+    # write's stream -- a write can never pick up another count's slabs (it takes the exact cold
+    # path instead), whatever happened to the ray buffer in between
     def count(self, rays, status=None, counters=None, stream=None, packed_info=None, stats=None):
         torch = _torch()
         n = rays.shape[0]
         dev = rays.device
         packed = packed_info if packed_info is not None else torch.empty((n, 2), dtype=torch.int64, device=dev)
         st = stats if stats is not None else torch.empty(STATS_LEN, dtype=torch.int64, device=dev)
-        _check(lib.sogk_sample_count(self._h, _ptr(rays), n, _ptr(packed), _ptr(st), _ptr(status),
-                                     _ptr(counters), _stream(stream)), "sample_count")
+        tok = _u64(0)
+        sh = _stream(stream)
+        _check(lib.sogk_sample_count_ex(self._h, _ptr(rays), n, _ptr(packed), _ptr(st), _ptr(status),
+                                        _ptr(counters), sh, C.byref(tok)), "sample_count")
+        self._tokens[_ptr(packed)] = (tok.value, _ptr(rays), n)
         return packed, st
 
     def write(self, rays, packed_info, total: int, ray_index_base: int = 0, stream=None,
@@ -541,9 +560,14 @@ class Sampler:
         lv = buf("levels", torch.uint8) if levels else None
         if total == 0:  # nothing to write (empty tensors have no device address)
             return ts, te, ri, ce, lv
-        _check(lib.sogk_sample_write(self._h, _ptr(rays), rays.shape[0], _ptr(packed_info),
-                                     ray_index_base, _ptr(ts), _ptr(te), _ptr(ri), _ptr(ce),
-                                     _ptr(lv), _stream(stream)), "sample_write")
+        sh = _stream(stream)
+        n = rays.shape[0]
+        tok, rp, tn = self._tokens.get(_ptr(packed_info), (0, None, -1))
+        if (rp, tn) != (_ptr(rays), n):
+            tok = 0  # packed_info was not filled by a count of these rays: exact cold path
+        _check(lib.sogk_sample_write_ex(self._h, _ptr(rays), n, _ptr(packed_info), tok,
+                                        ray_index_base, _ptr(ts), _ptr(te), _ptr(ri), _ptr(ce),
+                                        _ptr(lv), sh), "sample_write")
         return ts, te, ri, ce, lv
 
     def count_camera(self, cam: "Camera", first: int, n: int, packed_info, stats, stream=None,
@@ -561,15 +585,19 @@ class Sampler:
                                             _ptr(lv), _stream(stream)), "sample_write_camera")
 
     def sample(self, rays, ray_index_base: int = 0, stream=None, with_counters: bool = True) -> PackedSamples:
-        """Both passes on device rays (torch CUDA tensor [n, 8] float64)."""
+        """Both passes on device rays (torch CUDA tensor [n, 8] float64).  With `stream`, the
+        outputs are allocated on it and the total is read back in its order."""
         torch = _torch()
-        n = rays.shape[0]
-        status = torch.empty(n, dtype=torch.uint8, device=rays.device)
-        counters = torch.empty((n, 3), dtype=torch.int32, device=rays.device) if with_counters else None
-        packed, stats = self.count(rays, status, counters, stream)
-        hs = stats.cpu().numpy()
-        total = int(hs[STAT_TOTAL_SAMPLES])
-        ts, te, ri, ce, lv = self.write(rays, packed, total, ray_index_base, stream)
+        if stream is not None and not isinstance(stream, torch.cuda.Stream):
+            stream = torch.cuda.ExternalStream(int(_stream(stream)))
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            n = rays.shape[0]
+            status = torch.empty(n, dtype=torch.uint8, device=rays.device)
+            counters = torch.empty((n, 3), dtype=torch.int32, device=rays.device) if with_counters else None
+            packed, stats = self.count(rays, status, counters, stream)
+            hs = stats.cpu().numpy()  # on `stream` (the current stream here)
+            total = int(hs[STAT_TOTAL_SAMPLES])
+            ts, te, ri, ce, lv = self.write(rays, packed, total, ray_index_base, stream)
         return PackedSamples(packed, ts, te, ri, ce, lv, status, counters, hs)
 
     # -- host end-to-end API ------------------------------------------------

@@ -214,13 +214,30 @@ struct sogk_grid {
 struct Workspace {
     void* ptr = nullptr;
     size_t bytes = 0;
-    // the count whose slabs it holds: sampler id and the rays it ran on
+    // the count whose slabs it holds: its token (sogk_sample_count_ex), the sampler id and the
+    // rays / packed_info it ran on
+    uint64_t token = 0;
     uint64_t owner = 0;
+    const void* packed = nullptr;
     const void* rays = nullptr;
     int64_t first = -1, n = -1;
     bool cam = false;
 };
 static std::atomic<uint64_t> g_sampler_ids{0};
+static std::atomic<uint64_t> g_count_tokens{0};
+// Pass-1 slab budget per workspace: SOGK_SLAB_BUDGET_GB, else the larger of 8 GiB and 35 % of
+// the device memory free when first asked (a smaller slab only sends more rays to tail_kernel)
+static double slab_budget_bytes() {
+    static const double b = [] {
+        if (const char* e = std::getenv("SOGK_SLAB_BUDGET_GB")) return std::max(0.0, std::atof(e)) * double(1ull << 30);
+        size_t fr = 0, tot = 0;
+        double v = 8.0 * double(1ull << 30);
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) v = std::max(v, 0.35 * double(fr));
+        else cudaGetLastError();
+        return v;
+    }();
+    return b;
+}
 static std::mutex g_ws_mu;
 static std::map<std::pair<int, void*>, Workspace>& ws_registry() {
     static auto* m = new std::map<std::pair<int, void*>, Workspace>(); // never destroyed
@@ -243,6 +260,7 @@ static int workspace_for(void* stream, size_t need, Workspace** out) {
         w.ptr = nullptr;
         w.bytes = 0;
         w.owner = 0; // whatever it held is gone
+        w.token = 0;
         CK(cudaMalloc(&w.ptr, need), "sampler workspace");
         w.bytes = need;
     }
@@ -250,11 +268,82 @@ static int workspace_for(void* stream, size_t need, Workspace** out) {
     return SOGK_OK;
 }
 
+// Render scratch, one per (device, stream) like the workspaces (work on a stream is ordered;
+// the mutex covers host threads sharing a stream): [stats 256 B | packed n x 16 | rays n x 64]
+// and, per sample, t 8 B | ray index 4 B | shaded 32 B.
+struct RenderScratch {
+    static constexpr double kSampleBytes = 44.0;
+    std::mutex mu;
+    void* rb = nullptr;
+    int64_t rb_n = 0;
+    void* sb = nullptr;
+    int64_t smp_cap = 0;
+    int64_t* h_total = nullptr; // pinned
+    static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+    int ensure_rays(int64_t n) {
+        if (!h_total) CK(cudaMallocHost(&h_total, 64), "pinned total");
+        if (n <= rb_n && rb) return SOGK_OK;
+        cudaFree(rb); // synchronous: earlier frames that read it have finished
+        rb = nullptr;
+        rb_n = 0;
+        const int64_t m = std::max<int64_t>(n, 1);
+        CK(cudaMalloc(&rb, 256 + al(size_t(m) * 16) + size_t(m) * 64), "render scratch");
+        rb_n = m;
+        return SOGK_OK;
+    }
+    int ensure_samples(int64_t cap, void*) {
+        if (cap <= smp_cap && sb) return SOGK_OK;
+        cudaFree(sb);
+        sb = nullptr;
+        smp_cap = 0;
+        const int64_t m = std::max<int64_t>(cap, 1);
+        CK(cudaMalloc(&sb, al(size_t(m) * 8) + al(size_t(m) * 4) + size_t(m) * 32), "render sample scratch");
+        smp_cap = m;
+        return SOGK_OK;
+    }
+    int64_t* stats() const { return static_cast<int64_t*>(rb); }
+    int64_t* packed() const { return reinterpret_cast<int64_t*>(static_cast<char*>(rb) + 256); }
+    double* rays_buf() const {
+        return reinterpret_cast<double*>(static_cast<char*>(rb) + 256 + al(size_t(rb_n) * 16));
+    }
+    double* ts() const { return static_cast<double*>(sb); }
+    int32_t* ri() const { return reinterpret_cast<int32_t*>(static_cast<char*>(sb) + al(size_t(smp_cap) * 8)); }
+    void* shaded() const {
+        return static_cast<char*>(sb) + al(size_t(smp_cap) * 8) + al(size_t(smp_cap) * 4);
+    }
+    void release() {
+        cudaFree(rb);
+        cudaFree(sb);
+        if (h_total) cudaFreeHost(h_total);
+        rb = sb = nullptr;
+        h_total = nullptr;
+        rb_n = smp_cap = 0;
+    }
+};
+static std::map<std::pair<int, void*>, RenderScratch*>& render_registry() {
+    static auto* m = new std::map<std::pair<int, void*>, RenderScratch*>(); // never destroyed
+    return *m;
+}
+static RenderScratch* render_scratch_for(void* stream) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    RenderScratch*& r = render_registry()[{dev, stream}];
+    if (!r) r = new RenderScratch;
+    return r;
+}
+
 struct sogk_sampler {
     Variant v{};
     SamplerDev dev{};
     sogk_sampler_desc desc{};
     int n_levels = 0;
+    // the grids (immutable, caller-owned): launches on a stream first wait for their builds
+    const sogk_grid* lv[SOGK_MAX_LEVELS] = {};
+    int max_res = 0;
+    // serializes the calls that use per-sampler host state (sogk_sample_host, render): the
+    // reference's render_frame calls one make_sampler function from many threads
+    std::mutex host_mu;
     // sogk_sample_host scratch, pipeline streams and pinned per-chunk stats
     void* hb = nullptr;
     size_t hb_bytes = 0;
@@ -262,14 +351,9 @@ struct sogk_sampler {
     cudaStream_t lanes[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
     int64_t* h_chunk_stats = nullptr;
-    // sogk_render_camera scratch: stats (256 B) | packed [n][2] | rays [n][8] | t [T] | ray index [T] |
-    // shaded [T][4]
-    void* rb = nullptr;
-    size_t rb_bytes = 0;
 
     ~sogk_sampler() {
         cudaFree(hb);
-        cudaFree(rb);
         if (lanes_ready) {
             for (int l = 0; l < 3; ++l) {
                 cudaStreamDestroy(lanes[l]);
@@ -278,56 +362,29 @@ struct sogk_sampler {
             cudaFreeHost(h_chunk_stats);
         }
     }
-    static size_t ral(size_t x) { return (x + 255) & ~size_t(255); }
-    int ensure_render(int64_t n, int64_t total) {
-        const size_t need = 256 + ral(size_t(n) * 16) + ral(size_t(n) * 64) + ral(size_t(total) * 8) +
-                            ral(size_t(total) * 4) + size_t(total) * 32;
-        if (need > rb_bytes) {
-            void* nb = nullptr;
-            CK(cudaMalloc(&nb, need), "render scratch");
-            if (rb) { // keep stats + packed (pass 1 already wrote them)
-                cudaError_t e = cudaMemcpy(nb, rb, std::min(rb_bytes, 256 + ral(size_t(n) * 16)),
-                                           cudaMemcpyDeviceToDevice);
-                cudaFree(rb);
-                if (e != cudaSuccess) {
-                    cudaFree(nb);
-                    rb = nullptr;
-                    rb_bytes = 0;
-                    return cuda_fail(e, "render scratch");
-                }
-            }
-            rb = nb;
-            rb_bytes = need;
-        }
+
+    // order `stream` after the builds of every level (grids built on another stream: their
+    // pool storage and contents are valid in that stream's order only)
+    int wait_levels(void* stream) const {
+        for (int b = 0; b < n_levels; ++b)
+            if (lv[b] && lv[b]->ready) CK(cudaStreamWaitEvent(S(stream), lv[b]->ready, 0), "grid build wait");
         return SOGK_OK;
-    }
-    char* rbp() const { return static_cast<char*>(rb); }
-    int64_t* render_stats() const { return reinterpret_cast<int64_t*>(rbp()); }
-    int64_t* render_packed() const { return reinterpret_cast<int64_t*>(rbp() + 256); }
-    double* render_rays(int64_t n) const { return reinterpret_cast<double*>(rbp() + 256 + ral(size_t(n) * 16)); }
-    double* render_ts(int64_t n, int64_t) const {
-        return reinterpret_cast<double*>(rbp() + 256 + ral(size_t(n) * 16) + ral(size_t(n) * 64));
-    }
-    int32_t* render_ri(int64_t n, int64_t total) const {
-        return reinterpret_cast<int32_t*>(reinterpret_cast<char*>(render_ts(n, total)) + ral(size_t(total) * 8));
-    }
-    void* render_shaded(int64_t n, int64_t total) const {
-        return reinterpret_cast<char*>(render_ri(n, total)) + ral(size_t(total) * 4);
     }
 
     // pass 1 -> pass 2 handshake: the run slabs of a count live in the workspace of the
-    // (device, stream) it ran on, tagged with the sampler and the rays; a write on that stream
-    // by the same sampler on the same rays uses them, anything else takes the exact cold path
+    // (device, stream) it ran on, tagged with a token, the sampler and the rays; a write on that
+    // stream that presents the token (or, through the token-less API, the same sampler, rays and
+    // packed_info) uses them, anything else takes the exact cold path
     const uint64_t id = ++g_sampler_ids;
     int ray_order = 0; // 1: pass 1 processes buffer rays binned by entry cell and direction
     int64_t slab_cap = 128; // C: run records per ray (SOGK_SLAB; 0 = resume-only)
-    double slab_budget = 8.0 * (1ull << 30); // bytes of slabs per workspace (SOGK_SLAB_BUDGET_GB)
 
     int64_t cap_for(int64_t n) const {
         // keep the slabs within the budget; a smaller slab only sends more rays to
         // tail_kernel (exact either way)
+        const double budget = slab_budget_bytes();
         int64_t c = slab_cap;
-        while (c > 0 && double(n) * double(c) * 16.0 > slab_budget) c -= 4;
+        while (c > 0 && double(n) * double(c) * 16.0 > budget) c -= 4;
         return c < 0 ? 0 : c;
     }
     static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -345,22 +402,29 @@ struct sogk_sampler {
                al(e * sizeof(RunRec));
     }
     // the (device, stream) workspace, grown to fit n rays and tagged for this count
-    int claim_ws(int64_t n, void* stream, const void* rays, bool cam, int64_t first, Workspace** out) {
+    int claim_ws(int64_t n, void* stream, const void* rays, const void* packed, bool cam,
+                 int64_t first, Workspace** out) {
         Workspace* w = nullptr;
         int st = workspace_for(stream, need_bytes(n), &w);
         if (st) return st;
+        w->token = ++g_count_tokens;
         w->owner = id;
         w->rays = rays;
+        w->packed = packed;
         w->cam = cam;
         w->first = first;
         w->n = n;
         *out = w;
         return SOGK_OK;
     }
-    // the workspace holding this sampler's slabs for these rays, or nullptr
-    Workspace* owned_ws(void* stream, const void* rays, bool cam, int64_t first, int64_t n) const {
+    // the workspace holding this sampler's slabs for these rays, or nullptr; token != 0 must
+    // match the count's token, token == 0 (the token-less API) matches on the buffers
+    Workspace* owned_ws(void* stream, uint64_t token, const void* rays, const void* packed, bool cam,
+                        int64_t first, int64_t n) const {
         Workspace* w = workspace_peek(stream);
         if (!w || w->owner != id || w->n != n || w->cam != cam) return nullptr;
+        if (token) return w->token == token ? w : nullptr;
+        if (w->packed != packed) return nullptr;
         if (cam ? w->first != first : w->rays != rays) return nullptr;
         return w;
     }
@@ -374,7 +438,6 @@ struct sogk_sampler {
         char* p = static_cast<char*>(w->ptr) + scan_off(n);
         SlabDev S{};
         S.C = cap_for(n);
-        const size_t e = size_t(n) * size_t(S.C);
         S.resume = reinterpret_cast<Resume*>(p);
         p += al(resume_bytes(n));
         S.ovf_list = reinterpret_cast<uint32_t*>(p);
@@ -382,9 +445,29 @@ struct sogk_sampler {
         S.nruns = reinterpret_cast<int32_t*>(p);
         p += al(size_t(n) * 4);
         S.runs = reinterpret_cast<RunRec*>(p);
-        (void)e;
         S.ovf_ctr = ovf_ctr(w, n);
         return S;
+    }
+
+    // Upper bound on the samples of one camera ray (render scratch sizing without a host
+    // round trip), or -1 when none is cheap to state.  Every sample lies in the clipped range
+    // of the outermost level box, consecutive samples are >= dt0 - ulp(D)/2 apart (the ladder
+    // adds step(t) >= dt0 and rounds once, t <= D = the camera's farthest box corner).
+    int64_t max_points_per_camera_ray(const sogk_camera& c) const {
+        const GridDev& g = dev.lv[n_levels - 1];
+        double chord2 = 0.0, far2 = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            const double lo = g.wmin[a], hi = g.wmin[a] + double(g.res[a]) * g.voxel;
+            chord2 += (hi - lo) * (hi - lo);
+            const double f = std::max(std::fabs(c.position[a] - lo), std::fabs(c.position[a] - hi));
+            far2 += f * f;
+        }
+        const double D = std::sqrt(far2) * (1.0 + 1e-9) + 1.0;
+        const double ulpD = std::nextafter(D, DBL_MAX) - D;
+        if (!(ulpD < dev.dt0 * 0x1p-20) || !std::isfinite(D)) return -1;
+        const double m = dev.dt0 - ulpD;
+        const double k = std::floor(std::sqrt(chord2) * (1.0 + 1e-9) / m) + 2.0;
+        return k < 1e12 ? int64_t(k) : -1;
     }
 };
 
@@ -1023,8 +1106,11 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     s->v.branch = desc->kernel == SOGK_BRANCH ? 1 : 0;
     s->v.linear = desc->schedule == SOGK_LINEAR ? 1 : 0;
     if (const char* e = std::getenv("SOGK_SLAB")) s->slab_cap = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("SOGK_SLAB_BUDGET_GB")) s->slab_budget = std::max(0.0, std::atof(e)) * double(1ull << 30);
-    for (int b = 0; b < n_levels; ++b) s->dev.lv[b] = levels[b]->dev();
+    for (int b = 0; b < n_levels; ++b) {
+        s->dev.lv[b] = levels[b]->dev();
+        s->lv[b] = levels[b];
+        for (int a = 0; a < 3; ++a) s->max_res = std::max(s->max_res, levels[b]->t.res[a]);
+    }
     s->dev.n_levels = n_levels;
     s->dev.spin_cap = desc->spin_cap > 0 ? desc->spin_cap : SOGK_DEFAULT_SPIN_CAP;
     s->dev.dt0 = desc->dt0;
@@ -1048,6 +1134,10 @@ int sogk_release_workspaces(void) {
     CK(cudaDeviceSynchronize(), "release sync");
     for (auto& kv : ws_registry()) cudaFree(kv.second.ptr);
     ws_registry().clear();
+    for (auto& kv : render_registry()) {
+        std::lock_guard<std::mutex> r(kv.second->mu);
+        kv.second->release();
+    }
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
@@ -1084,16 +1174,20 @@ static CameraDev to_dev(const sogk_camera& c) {
 
 static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* cam,
                       int64_t first, int64_t n, int64_t* d_packed, int64_t* d_stats,
-                      uint8_t* d_status, int32_t* d_counters, void* stream, bool scan = true) {
+                      uint8_t* d_status, int32_t* d_counters, void* stream, uint64_t* token = nullptr) {
+    if (token) *token = 0;
     if (!s) return fail(SOGK_INVALID_ARG, "sampler is NULL");
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (n >= (int64_t(1) << 32)) return fail(SOGK_INVALID_ARG, "at most 2^32 - 1 rays per call");
     if (!d_stats) return fail(SOGK_INVALID_ARG, "stats buffer is NULL");
     if (n > 0 && (!d_packed || (!cam && !d_rays)))
         return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    int st = s->wait_levels(stream);
+    if (st) return st;
     CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
     if (n == 0) return SOGK_OK;
     Workspace* w = nullptr;
-    int st = s->claim_ws(n, stream, cam ? nullptr : d_rays, cam != nullptr, first, &w);
+    st = s->claim_ws(n, stream, cam ? nullptr : d_rays, d_packed, cam != nullptr, first, &w);
     if (st) return st;
     const int64_t tiles = scan_tiles(n);
     CK(cudaMemsetAsync(w->ptr, 0, size_t(tiles) * 8 + 64, S(stream)), "workspace reset");
@@ -1106,10 +1200,10 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
                     d_status, d_counters, slab, S(stream), perm),
        "count launch");
-    if (scan)
-        CK(launch_scan(n, d_packed, d_stats, sogk_sampler::tiles(w),
-                       reinterpret_cast<unsigned int*>(sogk_sampler::tiles(w) + tiles), S(stream)),
-           "scan launch");
+    CK(launch_scan(n, d_packed, d_stats, sogk_sampler::tiles(w),
+                   reinterpret_cast<unsigned int*>(sogk_sampler::tiles(w) + tiles), S(stream)),
+       "scan launch");
+    if (token) *token = w->token;
     return SOGK_OK;
 }
 
@@ -1124,6 +1218,13 @@ int sogk_sample_count(sogk_sampler* s, const double* d_rays, int64_t n, int64_t*
                       stream);
 }
 
+int sogk_sample_count_ex(sogk_sampler* s, const double* d_rays, int64_t n, int64_t* d_packed_info,
+                         int64_t* d_stats, uint8_t* d_status, int32_t* d_counters, void* stream,
+                         uint64_t* token) {
+    return count_impl(s, d_rays, nullptr, 0, n, d_packed_info, d_stats, d_status, d_counters,
+                      stream, token);
+}
+
 int sogk_sample_count_camera(sogk_sampler* s, const sogk_camera* cam, int64_t first_pixel,
                              int64_t n, int64_t* d_packed_info, int64_t* d_stats,
                              uint8_t* d_status, int32_t* d_counters, void* stream) {
@@ -1133,16 +1234,24 @@ int sogk_sample_count_camera(sogk_sampler* s, const sogk_camera* cam, int64_t fi
 }
 
 static int write_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* cam, int64_t first,
-                      int64_t n, const int64_t* d_packed, int64_t base, double* ts, double* te,
-                      int32_t* ri, uint32_t* ce, uint8_t* lv, void* stream) {
+                      int64_t n, const int64_t* d_packed, uint64_t token, int64_t base, double* ts,
+                      double* te, int32_t* ri, uint32_t* ce, uint8_t* lv, void* stream) {
     if (!s) return fail(SOGK_INVALID_ARG, "sampler is NULL");
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (n >= (int64_t(1) << 32)) return fail(SOGK_INVALID_ARG, "at most 2^32 - 1 rays per call");
+    if (ri && (base < 0 || base + n - 1 > int64_t(INT32_MAX)))
+        return fail(SOGK_INVALID_ARG, "ray_indices are int32: ray_index_base + n - 1 must be <= INT32_MAX");
+    if (ce && s->max_res > 1024)
+        return fail(SOGK_INVALID_ARG, "cells pack 10 bits per axis: grids above 1024 voxels per axis "
+                                      "cannot export cells");
     if (n == 0) return SOGK_OK;
     if (!d_packed || !ts || (!cam && !d_rays)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    int st = s->wait_levels(stream);
+    if (st) return st;
     CameraDev cd{};
     if (cam) cd = to_dev(*cam);
     // the slabs are valid when pass 1 ran on this sampler, stream and rays
-    const Workspace* w = s->owned_ws(stream, cam ? nullptr : d_rays, cam != nullptr, first, n);
+    const Workspace* w = s->owned_ws(stream, token, cam ? nullptr : d_rays, d_packed, cam != nullptr, first, n);
     const bool same = w != nullptr;
     const SlabDev slab = same ? s->slab(w, n) : SlabDev{};
     CK(launch_write(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed,
@@ -1155,8 +1264,16 @@ int sogk_sample_write(sogk_sampler* s, const double* d_rays, int64_t n,
                       const int64_t* d_packed_info, int64_t ray_index_base, double* d_t_starts,
                       double* d_t_ends, int32_t* d_ray_indices, uint32_t* d_cells,
                       uint8_t* d_levels, void* stream) {
-    return write_impl(s, d_rays, nullptr, 0, n, d_packed_info, ray_index_base, d_t_starts,
+    return write_impl(s, d_rays, nullptr, 0, n, d_packed_info, 0, ray_index_base, d_t_starts,
                       d_t_ends, d_ray_indices, d_cells, d_levels, stream);
+}
+
+int sogk_sample_write_ex(sogk_sampler* s, const double* d_rays, int64_t n,
+                         const int64_t* d_packed_info, uint64_t token, int64_t ray_index_base,
+                         double* d_t_starts, double* d_t_ends, int32_t* d_ray_indices,
+                         uint32_t* d_cells, uint8_t* d_levels, void* stream) {
+    return write_impl(s, d_rays, nullptr, 0, n, d_packed_info, token ? token : ~uint64_t(0),
+                      ray_index_base, d_t_starts, d_t_ends, d_ray_indices, d_cells, d_levels, stream);
 }
 
 int sogk_sample_write_camera(sogk_sampler* s, const sogk_camera* cam, int64_t first_pixel,
@@ -1164,7 +1281,7 @@ int sogk_sample_write_camera(sogk_sampler* s, const sogk_camera* cam, int64_t fi
                              double* d_t_starts, double* d_t_ends, int32_t* d_ray_indices,
                              uint32_t* d_cells, uint8_t* d_levels, void* stream) {
     if (!camera_range_ok(cam, first_pixel, n)) return fail(SOGK_INVALID_ARG, "pixel outside image");
-    return write_impl(s, nullptr, cam, first_pixel, n, d_packed_info, ray_index_base, d_t_starts,
+    return write_impl(s, nullptr, cam, first_pixel, n, d_packed_info, 0, ray_index_base, d_t_starts,
                       d_t_ends, d_ray_indices, d_cells, d_levels, stream);
 }
 
@@ -1303,29 +1420,59 @@ int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_came
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
     if (!camera_range_ok(cam, first_pixel, n)) return fail(SOGK_INVALID_ARG, "pixel outside image");
     if (!d_result && !d_rgb8) return fail(SOGK_INVALID_ARG, "NULL device buffer");
-    int st = s->ensure_render(n, 0);
+    std::lock_guard<std::mutex> hold(s->host_mu);
+    RenderScratch* rs = render_scratch_for(stream);
+    std::lock_guard<std::mutex> hold_rs(rs->mu);
+    int st = rs->ensure_rays(n);
     if (st) return st;
-    int64_t* stats = d_stats ? d_stats : s->render_stats();
-    // pass 1 + scan on the camera rays (rays generated in registers)
-    st = count_impl(s, nullptr, cam, first_pixel, n, s->render_packed(), stats, nullptr, nullptr, stream);
+    int64_t* stats = d_stats ? d_stats : rs->stats();
+    int64_t* packed = rs->packed();
+    // Sample capacity: the camera's bound when it fits in a quarter of free memory (allocated
+    // once per stream; the frame then runs without any host round trip), else the exact total
+    // read back after pass 1 (one sync), with geometric growth.
+    const bool force_sync = std::getenv("SOGK_RENDER_SYNC") != nullptr; // tests: the sync path
+    const int64_t per = force_sync ? -1 : s->max_points_per_camera_ray(*cam);
+    bool fixed = false;
+    if (per >= 0 && n > 0 && per <= INT64_MAX / 64 / n) {
+        const int64_t bound = per * n;
+        if (bound <= rs->smp_cap) {
+            fixed = true;
+        } else {
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) cudaGetLastError();
+            if (double(bound) * RenderScratch::kSampleBytes <= 0.25 * double(fr)) {
+                st = rs->ensure_samples(bound, stream);
+                if (st) return st;
+                fixed = true;
+            }
+        }
+    }
+    uint64_t tok = 0;
+    st = count_impl(s, nullptr, cam, first_pixel, n, packed, stats, nullptr, nullptr, stream, &tok);
     if (st) return st;
     if (n == 0) return SOGK_OK;
-    int64_t total = 0;
-    CK(cudaMemcpyAsync(&total, stats + SOGK_STAT_TOTAL_SAMPLES, 8, cudaMemcpyDeviceToHost, S(stream)), "total D2H");
-    CK(cudaStreamSynchronize(S(stream)), "count sync");
-    st = s->ensure_render(n, total);
-    if (st) return st;
+    int64_t hint = rs->smp_cap;
+    if (!fixed) {
+        CK(cudaMemcpyAsync(rs->h_total, stats + SOGK_STAT_TOTAL_SAMPLES, 8, cudaMemcpyDeviceToHost, S(stream)),
+           "total D2H");
+        CK(cudaStreamSynchronize(S(stream)), "count sync");
+        hint = *rs->h_total;
+        if (hint > rs->smp_cap) {
+            st = rs->ensure_samples(hint + hint / 2, stream);
+            if (st) return st;
+        }
+    }
     // pass 2 (t_starts, ray_indices), the ray buffer for shading, then shade + accumulate
-    if (total > 0) {
-        st = write_impl(s, nullptr, cam, first_pixel, n, s->render_packed(), 0, s->render_ts(n, total),
-                        nullptr, s->render_ri(n, total), nullptr, nullptr, stream);
+    if (hint > 0) {
+        st = write_impl(s, nullptr, cam, first_pixel, n, packed, tok, 0, rs->ts(), nullptr, rs->ri(),
+                        nullptr, nullptr, stream);
         if (st) return st;
     }
     const CameraDev cd = to_dev(*cam);
-    CK(launch_raygen(cd, first_pixel, n, s->render_rays(n), S(stream)), "raygen");
-    CK(launch_shade_accumulate(s->v, s->dev, scene->dev, s->render_rays(n), n, s->render_packed(),
-                               s->render_ts(n, total), s->render_ri(n, total), total, 0,
-                               s->render_shaded(n, total), d_result, d_rgb8, S(stream)),
+    CK(launch_raygen(cd, first_pixel, n, rs->rays_buf(), S(stream)), "raygen");
+    CK(launch_shade_accumulate(s->v, s->dev, scene->dev, rs->rays_buf(), n, packed, rs->ts(), rs->ri(),
+                               stats + SOGK_STAT_TOTAL_SAMPLES, hint, 0, rs->shaded(), d_result, d_rgb8,
+                               S(stream)),
        "render shade");
     return SOGK_OK;
 }
@@ -1369,6 +1516,9 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     if (!s || !h_stats) return fail(SOGK_INVALID_ARG, "NULL argument");
     if (n < 0 || capacity < 0) return fail(SOGK_INVALID_ARG, "negative size");
     if (n > 0 && (!h_rays || !h_packed_info)) return fail(SOGK_INVALID_ARG, "NULL host buffer");
+    if (h_ray_indices && (ray_index_base < 0 || ray_index_base + n - 1 > int64_t(INT32_MAX)))
+        return fail(SOGK_INVALID_ARG, "ray_indices are int32: ray_index_base + n - 1 must be <= INT32_MAX");
+    std::lock_guard<std::mutex> hold(s->host_mu); // per-sampler scratch, lanes and pinned stats
     // Chunked pipeline over kLanes internal streams: chunk c's upload and pass 1 overlap the
     // pass 2 and download of chunk c-1 (each stream has its own pass-1 -> pass-2 workspace).
     // Offsets are made global on the device before download; the call is synchronous.
@@ -1433,6 +1583,7 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
 
     for (int k = 0; k < SOGK_STATS_LEN; ++k) h_stats[k] = 0;
     std::vector<int64_t> chunk_stats(size_t(nchunks) * SOGK_STATS_LEN, 0);
+    std::vector<uint64_t> tokens(size_t(nchunks), 0);
     int64_t base = 0;
     bool fits = true;
     int rc = SOGK_OK;
@@ -1443,7 +1594,7 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         CK(cudaMemcpyAsync(d_rays + 8 * r0, h_rays + 8 * r0, size_t(m) * 64, cudaMemcpyHostToDevice, L), "rays H2D");
         const int st = count_impl(s, d_rays + 8 * r0, nullptr, 0, m, d_packed + 2 * r0,
                                   d_stats + c * SOGK_STATS_LEN, h_status ? d_status + r0 : nullptr,
-                                  h_counters ? d_ctr + 3 * r0 : nullptr, L);
+                                  h_counters ? d_ctr + 3 * r0 : nullptr, L, &tokens[size_t(c)]);
         if (st) return st;
         int64_t* hs = s->h_chunk_stats + (c % 64) * SOGK_STATS_LEN;
         CK(cudaMemcpyAsync(hs, d_stats + c * SOGK_STATS_LEN, SOGK_STATS_LEN * 8, cudaMemcpyDeviceToHost, L), "stats D2H");
@@ -1462,7 +1613,7 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         if (fits && base + tot <= capacity) {
             if (tot > 0) {
                 const int st = write_impl(s, d_rays + 8 * r0, nullptr, 0, m, d_packed + 2 * r0,
-                                          ray_index_base + r0, d_ts, h_t_ends ? d_te : nullptr,
+                                          tokens[size_t(c)], ray_index_base + r0, d_ts, h_t_ends ? d_te : nullptr,
                                           h_ray_indices ? d_ri : nullptr, h_cells ? d_ce : nullptr,
                                           h_levels ? d_lv : nullptr, L);
                 if (st) return st;

@@ -73,11 +73,13 @@ cudaError_t launch_composite(const Variant& v, const SamplerDev& s, const SceneD
                              double* result, uint8_t* rgb8, cudaStream_t st);
 // frame compositing after pass 1 + scan + gather: per-sample shading (32 B each into
 // `shaded`), then the per-ray front-to-back sums
+// (grid-stride over *d_total samples, read on the device; total_hint sizes the grid: the
+// exact total when known on the host, else the sample capacity)
 cudaError_t launch_shade_accumulate(const Variant& v, const SamplerDev& s, const SceneDev& sc,
                                     const double* rays, int64_t n, const int64_t* packed,
-                                    const double* ts, const int32_t* ri, int64_t total,
-                                    int64_t ray_index_base, void* shaded, double* result,
-                                    uint8_t* rgb8, cudaStream_t st);
+                                    const double* ts, const int32_t* ri, const int64_t* d_total,
+                                    int64_t total_hint, int64_t ray_index_base, void* shaded,
+                                    double* result, uint8_t* rgb8, cudaStream_t st);
 
 
 // packed_info[r].offset += base for r < n

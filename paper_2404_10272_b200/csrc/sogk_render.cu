@@ -14,6 +14,8 @@
 // within a tolerance, not bit for bit (tests/test_gpu_render.py states it).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "sogk_device.cuh"
 #include "sogk_internal.h"
 #include "sogk_sources.cuh"
@@ -152,11 +154,14 @@ __global__ void __launch_bounds__(kRenderBlock)
 template <int SCH>
 __global__ void __launch_bounds__(kRenderBlock)
     shade_kernel(const __grid_constant__ SamplerDev s, const SceneDev sc, const double* rays,
-                 int64_t total, const int64_t* __restrict__ packed, const double* __restrict__ ts,
-                 const int32_t* __restrict__ ri, int64_t ray_index_base,
-                 double4* __restrict__ shaded) {
-    const int64_t e = (int64_t)blockIdx.x * kRenderBlock + threadIdx.x;
-    if (e >= total) return;
+                 const int64_t* __restrict__ d_total, const int64_t* __restrict__ packed,
+                 const double* __restrict__ ts, const int32_t* __restrict__ ri,
+                 int64_t ray_index_base, double4* __restrict__ shaded) {
+    // grid-stride over the frame's samples; the total comes from pass 1 on the device, so the
+    // host never waits for it
+    const int64_t total = *d_total;
+    for (int64_t e = (int64_t)blockIdx.x * kRenderBlock + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * kRenderBlock) {
     const int64_t r = __ldg(ri + e) - ray_index_base;
     const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
     const double t = __ldg(ts + e);
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(kRenderBlock)
         out = make_double4(1.0 - exp(-sigma * dt), em[0] / sigma, em[1] / sigma, em[2] / sigma);
     }
     shaded[e] = out;
+    }
 }
 
 __global__ void __launch_bounds__(kRenderBlock)
@@ -203,17 +209,25 @@ __global__ void __launch_bounds__(kRenderBlock)
 
 cudaError_t launch_shade_accumulate(const Variant& v, const SamplerDev& s, const SceneDev& sc,
                                     const double* rays, int64_t n, const int64_t* packed,
-                                    const double* ts, const int32_t* ri, int64_t total,
-                                    int64_t ray_index_base, void* shaded, double* result,
-                                    uint8_t* rgb8, cudaStream_t st) {
-    if (total > 0) {
-        const unsigned blocks = (unsigned)((total + kRenderBlock - 1) / kRenderBlock);
+                                    const double* ts, const int32_t* ri, const int64_t* d_total,
+                                    int64_t total_hint, int64_t ray_index_base, void* shaded,
+                                    double* result, uint8_t* rgb8, cudaStream_t st) {
+    if (total_hint > 0) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
+        const int64_t want = (total_hint + kRenderBlock - 1) / kRenderBlock;
+        const unsigned blocks = (unsigned)std::min<int64_t>(want, int64_t(sms) * 16);
         if (v.linear)
-            shade_kernel<1><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, total, packed, ts, ri, ray_index_base,
-                                                            static_cast<double4*>(shaded));
+            shade_kernel<1><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, d_total, packed, ts, ri,
+                                                            ray_index_base, static_cast<double4*>(shaded));
         else
-            shade_kernel<0><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, total, packed, ts, ri, ray_index_base,
-                                                            static_cast<double4*>(shaded));
+            shade_kernel<0><<<blocks, kRenderBlock, 0, st>>>(s, sc, rays, d_total, packed, ts, ri,
+                                                            ray_index_base, static_cast<double4*>(shaded));
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -84,13 +84,14 @@ __device__ __forceinline__ long long block_sum(long long v) {
     return t;
 }
 
-// resume state at `run`; tag bits 8.. carry the number of samples already in the slab
-__device__ __forceinline__ void store_resume(Resume* dst, const Run& run, int filled) {
+// resume state at `run`; tag bits 8..31 carry the number of samples already in the slab
+// (filled <= kRunStartMax = 2^24 - 1: packed and unpacked as unsigned, never sign-extended)
+__device__ __forceinline__ void store_resume(Resume* dst, const Run& run, uint32_t filled) {
     Resume r;
     r.ijk[0] = run.ijk[0];
     r.ijk[1] = run.ijk[1];
     r.ijk[2] = run.ijk[2];
-    r.tag = run.tag | (filled << 8);
+    r.tag = (int)(((uint32_t)run.tag & 255u) | (filled << 8));
     r.t_cur = run.t0;
     r.t_last = run.t_last0;
     *dst = r;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MIN
                     run.tag = gen.an.resume_tag();
                     run.t0 = ev.t0;
                     run.t_last0 = t_last0;
-                    store_resume(S.resume + r, run, (int)filled);
+                    store_resume(S.resume + r, run, (uint32_t)filled);
                 }
             }
             // run count; bit 31 marks a ray whose runs overflowed the slab
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kGather)
         s_off[tid] = pi.x;
         // every sample of the ray is in its runs, unless they overflowed the slab: then the
         // slab covers the samples before the resume point (Resume::tag >> 8)
-        s_fill[tid] = raw < 0 ? (S.resume[r].tag >> 8) : (int)pi.y;
+        s_fill[tid] = raw < 0 ? (int)((uint32_t)S.resume[r].tag >> 8) : (int)pi.y;
     }
     s_nr[tid] = nr;
     // block exclusive scan of the run counts
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(kWriteBlock)
         const int64_t r = S.ovf_list[i];
         const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
         Resume res = S.resume[r];
-        const long long skip = res.tag >> 8;
+        const long long skip = (long long)((uint32_t)res.tag >> 8);
         res.tag &= 255;
         RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
         gen.init(src.load(r), s);

@@ -83,3 +83,32 @@ def assert_packed_equal(got: Packed, want: Packed, what: str = "", counters: boo
         badc = np.nonzero((got.counters != want.counters).any(axis=1))[0]
         assert badc.size == 0, (f"{what}: counters differ on {badc.size} rays, first {badc[:5]}: "
                                 f"got {got.counters[badc[:3]].tolist()} want {want.counters[badc[:3]].tolist()}")
+
+
+def ref_sample(reflib, levels, analyzer, kernel, sched, rays, cascade=False, skip=None) -> Packed:
+    """The unmodified reference (oracle/_ref: sog::run_sampler / run_cascade_sampler per ray on
+    all host threads); rays with skip != 0 are not run (status 2, no samples)."""
+    s = reflib.sampler(levels, analyzer, kernel, sched.kind, sched.dt0, sched.growth, cascade=cascade)
+    return s.sample(rays, skip=skip)
+
+
+def assert_rays_equal(got: Packed, want: Packed, mask, what: str = "", counters: bool = True,
+                      cells: bool = True, ray_index_base: int = 0):
+    """Per-ray comparison on the rays where mask is True (e.g. not spin-screened): counts,
+    t_starts, t_ends, ray_indices, cells, levels (and counters) bit for bit."""
+    mask = np.asarray(mask, bool)
+    gc, wc = got.packed_info[:, 1], want.packed_info[:, 1]
+    bad = np.nonzero(mask & (gc != wc))[0]
+    assert bad.size == 0, f"{what}: counts differ on {bad.size} rays, first {bad[:5]}: {gc[bad[:3]]} vs {wc[bad[:3]]}"
+    gsel = np.repeat(mask, gc)
+    wsel = np.repeat(mask, wc)
+    assert np.array_equal(bits64(got.t_starts)[gsel], bits64(want.t_starts)[wsel]), f"{what}: t_starts differ"
+    assert np.array_equal(bits64(got.t_ends)[gsel], bits64(want.t_ends)[wsel]), f"{what}: t_ends differ"
+    ri = np.repeat(np.arange(gc.size, dtype=np.int64) + ray_index_base, gc).astype(np.int32)
+    assert np.array_equal(got.ray_indices, ri), f"{what}: ray_indices differ"
+    if cells:
+        assert np.array_equal(got.cells[gsel], want.cells[wsel]), f"{what}: cells differ"
+        assert np.array_equal(got.levels[gsel], want.levels[wsel]), f"{what}: levels differ"
+    if counters and want.counters is not None:
+        badc = np.nonzero(mask & (got.counters != want.counters).any(axis=1))[0]
+        assert badc.size == 0, f"{what}: counters differ on {badc.size} rays, first {badc[:5]}"
