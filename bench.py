@@ -82,6 +82,65 @@ def orbit_pos(view: int):
     return (x * math.cos(th) + z * math.sin(th), y, -x * math.sin(th) + z * math.cos(th))
 
 
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled through NVML every 5 ms while the timed region runs
+    (nvidia-smi's own polling starts too slowly for a sub-second region); falls back to
+    `nvidia-smi -lms` when NVML is unavailable."""
+
+    # nvmlClocksEventReasons bits (nvml.h)
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.rows.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), int(get_r(h))))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+        except Exception:
+            self.t = None
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.t is not None:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, m in self.rows for b, name in self.BITS.items() if m & b})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml"}
+
+
 def workload_config(name: str, world: int, streams: int) -> dict:
     """The bench line's `config`, identical in both arms (it depends on the arguments only)."""
     if name == "cfg2":

@@ -234,6 +234,51 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
                      uint8_t* h_levels, uint8_t* h_status, int32_t* h_counters,
                      int64_t* h_stats, void* stream);
 
+/* ---- traverse ----------------------------------------------------------
+ * The analyzers' event streams (the reference's traverse entry points): for every ray, the
+ * events DdaTraversal / HddaTraversal / CdTraversal / CascadeTraversal::next() return until
+ * the stream ends, i.e. collect_events (traversal.hpp:120-264, 270-359; sampling.hpp:305-415),
+ * plus lookup_count() / step_count() after the last event.  The sampler handle supplies the
+ * grids, the analyzer, the cascade flag and the spin cap; its kernel and schedule are unused.
+ * Rays the reference never returns on (HddaTraversal / CdTraversal edge-crossing spin) get
+ * status SOGK_RAY_UNDEFINED and no events; invalid rays SOGK_RAY_INVALID. */
+/* sog::TraversalEvent (grid.hpp:98-104) / sog::CascadeEvent (sampling.hpp:297-299) */
+typedef struct {
+    int32_t ijk[3];     /* lowest voxel of the node (voxel for DDA, node origin for HDDA / CD) */
+    int32_t level;      /* sog::Level (grid.hpp:75) */
+    double t0, t1;      /* [t0, t1); consecutive events share the boundary exactly */
+    int32_t occupied;
+    int32_t grid_level; /* cascade level, -1 outside every level; 0 for a single grid */
+} sogk_event;
+/* pass 1: per-ray event counts scanned into d_event_info[n][2] = {offset, count}; d_stats:
+ * SOGK_STAT_TOTAL_SAMPLES holds the event total, _ANALYZER_LOOKUPS / _STEPS and
+ * _INVALID_RAYS / _UNDEFINED_RAYS as for sampling.  d_status (uint8[n]) and d_counters
+ * (int32[n][2] = lookup_count, step_count) are optional. */
+int sogk_traverse_count(sogk_sampler* s, const double* d_rays, int64_t n, int64_t* d_event_info,
+                        int64_t* d_stats, uint8_t* d_status, int32_t* d_counters, void* stream);
+/* pass 2: the events of every ray at its d_event_info offset (d_events holds the total) */
+int sogk_traverse_write(sogk_sampler* s, const double* d_rays, int64_t n,
+                        const int64_t* d_event_info, sogk_event* d_events, void* stream);
+/* both passes from host buffers (synchronous); SOGK_INSUFFICIENT_CAPACITY when the event
+ * total exceeds `capacity` (h_stats and h_event_info are filled) */
+int sogk_traverse_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t capacity,
+                       int64_t* h_event_info, sogk_event* h_events, uint8_t* h_status,
+                       int32_t* h_counters, int64_t* h_stats, void* stream);
+
+/* sog::QueryResult (sparse.hpp:130-135) */
+typedef struct {
+    int32_t occupied;
+    int32_t level;      /* sog::Level */
+    int32_t origin[3];  /* lowest voxel of the uniform node that answered */
+    int32_t extent;     /* 1, 8 or 128 */
+} sogk_query;
+/* SparseGrid::query (sparse.hpp:163-171) for a VDB grid (out of bounds: the empty root tile
+ * of the 128-aligned region); DenseGrid::voxel_at (grid.hpp:129-133) as a leaf_voxel answer
+ * for a dense grid.  d_ijk: int32[n][3]. */
+int sogk_grid_query(const sogk_grid* g, const int32_t* d_ijk, int64_t n, sogk_query* d_out,
+                    void* stream);
+int sogk_grid_query_host(const sogk_grid* g, const int32_t* h_ijk, int64_t n, sogk_query* h_out);
+
 /* ---- rays -------------------------------------------------------------- */
 /* host: Camera::pixel_ray's per-camera terms (camera.hpp:158-173) */
 int sogk_camera_setup(const double position[3], const double target[3], const double up[3],

@@ -289,6 +289,106 @@ inline std::function<SampleRun(const Ray&)> make_sampler(const Sampler& s) {
     return [s](const Ray& r) { return s(r); };
 }
 
+/// Event streams of a ray batch (the reference's traverse entry points, traversal.hpp:120-359):
+/// ray r's events exactly as collect_events(Analyzer(grid, ray)) returns them, and the
+/// analyzer's lookup_count() / step_count() after the last one.
+struct EventStreams {
+    std::vector<std::int64_t> event_info; // [n][2] offset, count
+    std::vector<sogk_event> events;
+    std::vector<std::uint8_t> status;     // SOGK_RAY_OK / _INVALID / _UNDEFINED
+    std::vector<std::int32_t> counters;   // [n][2] lookup_count, step_count
+    std::int64_t stats[SOGK_STATS_LEN] = {};
+
+    std::size_t size() const { return event_info.size() / 2; }
+    static TraversalEvent to_ref(const sogk_event& e) {
+        TraversalEvent t;
+        t.ijk = Vec3i{e.ijk[0], e.ijk[1], e.ijk[2]};
+        t.level = static_cast<Level>(e.level);
+        t.t0 = e.t0;
+        t.t1 = e.t1;
+        t.occupied = e.occupied != 0;
+        return t;
+    }
+    /// collect_events of ray r (traversal.hpp:339-343)
+    std::vector<TraversalEvent> ray_events(std::size_t r) const {
+        std::vector<TraversalEvent> out;
+        for (std::int64_t k = 0; k < event_info[2 * r + 1]; ++k)
+            out.push_back(to_ref(events[std::size_t(event_info[2 * r] + k)]));
+        return out;
+    }
+    /// the CascadeTraversal events of ray r (sampling.hpp:297-299): grid_level included
+    std::vector<CascadeEvent> ray_cascade_events(std::size_t r) const {
+        std::vector<CascadeEvent> out;
+        for (std::int64_t k = 0; k < event_info[2 * r + 1]; ++k) {
+            const sogk_event& e = events[std::size_t(event_info[2 * r] + k)];
+            CascadeEvent c;
+            static_cast<TraversalEvent&>(c) = to_ref(e);
+            c.grid_level = e.grid_level;
+            out.push_back(c);
+        }
+        return out;
+    }
+    long lookup_count(std::size_t r) const { return counters[2 * r]; }
+    long step_count(std::size_t r) const { return counters[2 * r + 1]; }
+};
+
+/// DdaTraversal / HddaTraversal / CdTraversal / CascadeTraversal (traversal.hpp:120-337,
+/// sampling.hpp:305-415) over ray batches on the GPU: the analyzer is the grid's
+/// (dense -> DDA, VDB -> HDDA, distance -> CD; a vector of levels -> the cascade).
+class Traverser {
+public:
+    template <class G>
+    explicit Traverser(const G& grid) : s_(grid, KernelKind::skip, StepSchedule::constant(1.0)) {}
+
+    EventStreams traverse_rays(std::span<const Ray> rays, void* stream = nullptr) const {
+        const std::int64_t n = std::int64_t(rays.size());
+        EventStreams out;
+        out.event_info.resize(2 * n);
+        out.status.resize(n);
+        out.counters.resize(2 * n);
+        std::int64_t cap = std::max<std::int64_t>(256, 64 * n);
+        for (;;) {
+            out.events.resize(std::size_t(cap));
+            const int st = sogk_traverse_host(s_.handle(), reinterpret_cast<const double*>(rays.data()), n,
+                                              cap, out.event_info.data(), out.events.data(), out.status.data(),
+                                              out.counters.data(), out.stats, stream);
+            if (st == SOGK_INSUFFICIENT_CAPACITY) {
+                cap = out.stats[SOGK_STAT_TOTAL_SAMPLES];
+                continue;
+            }
+            check(st);
+            break;
+        }
+        out.events.resize(std::size_t(out.stats[SOGK_STAT_TOTAL_SAMPLES]));
+        return out;
+    }
+
+    /// collect_events(Analyzer(grid, ray)) for one ray; the reference's next() never returns
+    /// on the edge-crossing spin rays: those throw instead of hanging
+    std::vector<TraversalEvent> collect_events(const Ray& ray) const {
+        const EventStreams e = traverse_rays({&ray, 1});
+        if (e.status[0] == SOGK_RAY_UNDEFINED)
+            throw std::runtime_error("the reference analyzer never returns on this ray (edge-crossing spin)");
+        return e.ray_events(0);
+    }
+
+private:
+    Sampler s_;
+};
+
+/// SparseGrid::query (sparse.hpp:163-171) on the GPU, one point
+inline QueryResult query(const DeviceSparseGrid& g, const Vec3i& ijk) {
+    const std::int32_t p[3] = {ijk.x, ijk.y, ijk.z};
+    sogk_query q{};
+    check(sogk_grid_query_host(g.handle(), p, 1, &q));
+    QueryResult r;
+    r.occupied = q.occupied != 0;
+    r.level = static_cast<Level>(q.level);
+    r.origin = Vec3i{q.origin[0], q.origin[1], q.origin[2]};
+    r.extent = q.extent;
+    return r;
+}
+
 /// AnalyticScene (render.hpp:58-92) in HBM.
 class DeviceScene {
 public:

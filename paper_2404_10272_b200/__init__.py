@@ -44,7 +44,8 @@ __all__ = [
     "run_cascade_sampler", "make_sampler", "Camera", "generate_scene", "build_dense_cascade",
     "make_probe_rays", "random_rays", "random_grid", "random_blocky_grid", "serialize_dense",
     "serialize_sparse", "deserialize_dense", "deserialize_sparse", "memory_bytes", "IoError",
-    "SceneKind", "RAY_OK", "RAY_INVALID", "RAY_UNDEFINED",
+    "SceneKind", "RAY_OK", "RAY_INVALID", "RAY_UNDEFINED", "Traversal", "collect_events",
+    "dump_trace", "query", "EVENT_DTYPE", "QUERY_DTYPE",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -55,6 +56,15 @@ RAY_OK, RAY_INVALID, RAY_UNDEFINED = 0, 1, 2
 STATS_LEN = 8
 (STAT_TOTAL_SAMPLES, STAT_INVALID_RAYS, STAT_UNDEFINED_RAYS, STAT_ANALYZER_LOOKUPS,
  STAT_ANALYZER_STEPS, STAT_KERNEL_LOOKUPS, STAT_SLAB_OVERFLOW_RAYS) = range(7)
+
+
+# sogk_event = sog::TraversalEvent / CascadeEvent (grid.hpp:98-104, sampling.hpp:297-299)
+EVENT_DTYPE = np.dtype([("ijk", np.int32, 3), ("level", np.int32), ("t0", np.float64), ("t1", np.float64),
+                        ("occupied", np.int32), ("grid_level", np.int32)])
+# sogk_query = sog::QueryResult (sparse.hpp:130-135)
+QUERY_DTYPE = np.dtype([("occupied", np.int32), ("level", np.int32), ("origin", np.int32, 3),
+                        ("extent", np.int32)])
+LEVEL_NAMES = ("leaf_voxel", "leaf_tile", "internal_tile", "root_tile")  # level_name (grid.hpp:84-91)
 
 
 class IoError(RuntimeError):
@@ -125,6 +135,11 @@ _SIGS = {
     "sogk_sample_count_camera": (C.c_int, [_vp, C.POINTER(_Camera), _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_write_camera": (C.c_int, [_vp, C.POINTER(_Camera), _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sogk_sample_host": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "sogk_traverse_count": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "sogk_traverse_write": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
+    "sogk_traverse_host": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "sogk_grid_query": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "sogk_grid_query_host": (C.c_int, [_vp, _vp, _i64, _vp]),
     "sogk_camera_setup": (C.c_int, [_vp, _vp, _vp, _dbl, _i32, _i32, _dbl, C.POINTER(_Camera)]),
     "sogk_camera_rays": (C.c_int, [C.POINTER(_Camera), _i64, _i64, _vp, _vp]),
     "sogk_camera_rays_host": (C.c_int, [C.POINTER(_Camera), _i64, _i64, _vp]),
@@ -598,7 +613,52 @@ class Sampler:
             hs = stats.cpu().numpy()  # on `stream` (the current stream here)
             total = int(hs[STAT_TOTAL_SAMPLES])
             ts, te, ri, ce, lv = self.write(rays, packed, total, ray_index_base, stream)
+        if stream is not None:  # outputs usable in the caller's stream order
+            torch.cuda.current_stream().wait_stream(stream)
         return PackedSamples(packed, ts, te, ri, ce, lv, status, counters, hs)
+
+    # -- traverse (the analyzers' event streams) ----------------------------
+    def traverse(self, rays, stream=None) -> "Traversal":
+        """collect_events of every ray on the device (sogk_traverse_count / _write): torch
+        tensors event_info [n, 2] (offset, count), events (uint8 [total, 40], view with
+        EVENT_DTYPE), status, counters [n, 2] (lookup_count, step_count)."""
+        torch = _torch()
+        n = rays.shape[0]
+        dev = rays.device
+        info = torch.empty((n, 2), dtype=torch.int64, device=dev)
+        stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
+        status = torch.empty(n, dtype=torch.uint8, device=dev)
+        counters = torch.empty((n, 2), dtype=torch.int32, device=dev)
+        sh = _stream(stream)
+        _check(lib.sogk_traverse_count(self._h, _ptr(rays), n, _ptr(info), _ptr(stats), _ptr(status),
+                                       _ptr(counters), sh), "traverse_count")
+        with torch.cuda.stream(torch.cuda.ExternalStream(sh)) if sh else _nullctx():
+            hs = stats.cpu().numpy()
+        total = int(hs[STAT_TOTAL_SAMPLES])
+        events = torch.empty((max(total, 1), EVENT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        if total:
+            _check(lib.sogk_traverse_write(self._h, _ptr(rays), n, _ptr(info), _ptr(events), sh),
+                   "traverse_write")
+        return Traversal(info, events[:total], status, counters, hs)
+
+    def traverse_host(self, rays: np.ndarray, stream=None) -> "Traversal":
+        """The same from host rays (sogk_traverse_host): numpy outputs, events as EVENT_DTYPE."""
+        rays = np.ascontiguousarray(rays, np.float64).reshape(-1, 8)
+        n = rays.shape[0]
+        cap = max(64, 64 * n)
+        while True:
+            info = np.zeros((n, 2), np.int64)
+            ev = np.zeros(cap, EVENT_DTYPE)
+            st = np.zeros(n, np.uint8)
+            ct = np.zeros((n, 2), np.int32)
+            stats = np.zeros(STATS_LEN, np.int64)
+            rc = lib.sogk_traverse_host(self._h, _ptr(rays), n, cap, _ptr(info), ev.ctypes.data, _ptr(st),
+                                        _ptr(ct), _ptr(stats), _stream(stream))
+            if rc == INSUFFICIENT_CAPACITY:
+                cap = int(stats[STAT_TOTAL_SAMPLES])
+                continue
+            _check(rc, "traverse_host")
+            return Traversal(info, ev[:int(stats[STAT_TOTAL_SAMPLES])], st, ct, stats)
 
     # -- host end-to-end API ------------------------------------------------
     def sample_host(self, rays: np.ndarray, ray_index_base: int = 0, capacity: Optional[int] = None,
@@ -627,6 +687,65 @@ class Sampler:
             _check(rc, "sample_host")
             tot = int(stats[STAT_TOTAL_SAMPLES])
             return PackedSamples(pi, ts[:tot], te[:tot], ri[:tot], ce[:tot], lv[:tot], stt, ct, stats)
+
+
+@dataclass
+class Traversal:
+    """Event streams of a ray batch: ray r's events are events[info[r,0] : info[r,0] + info[r,1]];
+    counters[r] = (lookup_count, step_count) after its last event (traversal.hpp:120-264)."""
+
+    event_info: object
+    events: object
+    status: object
+    counters: object
+    stats: Optional[np.ndarray] = None
+
+    def host_events(self) -> np.ndarray:
+        ev = self.events
+        if hasattr(ev, "cpu"):
+            ev = ev.cpu().numpy()
+        return np.ascontiguousarray(ev).reshape(-1).view(np.uint8).view(EVENT_DTYPE)
+
+    def ray_events(self, r: int) -> np.ndarray:
+        info = self.event_info.cpu().numpy() if hasattr(self.event_info, "cpu") else self.event_info
+        o, c = info[r]
+        return self.host_events()[o:o + c]
+
+
+def dump_trace(events) -> str:
+    """dump_trace (traversal.hpp:345-357): level, ijk, t0, t1 (%.17g), occupied per line."""
+    out = []
+    for e in events:
+        i = e["ijk"]
+        out.append(f"{LEVEL_NAMES[int(e['level'])]}\t{int(i[0])},{int(i[1])},{int(i[2])}\t"
+                   f"{float(e['t0']):.17g}\t{float(e['t1']):.17g}\t{1 if e['occupied'] else 0}\n")
+    return "".join(out)
+
+
+def collect_events(grid_or_levels, ray, cascade: bool = False, spin_cap: int = 0):
+    """collect_events(Analyzer(grid, ray)) (traversal.hpp:339-343) for one ray: DdaTraversal on a
+    DenseGrid, HddaTraversal on a SparseGrid, CdTraversal on a DistanceGrid, CascadeTraversal on
+    a list of levels -> (events [EVENT_DTYPE], lookup_count, step_count)."""
+    levels = list(grid_or_levels) if isinstance(grid_or_levels, (list, tuple)) else [grid_or_levels]
+    an = (Analyzer.hdda if isinstance(levels[0], SparseGrid) else
+          Analyzer.cd if isinstance(levels[0], DistanceGrid) else Analyzer.dda)
+    s = Sampler(levels, an, KernelKind.skip, StepSchedule.constant(1.0),
+                cascade=cascade or len(levels) > 1, spin_cap=spin_cap)
+    t = s.traverse_host(np.asarray(_ray_array(Ray.coerce(ray)), np.float64).reshape(1, 8))
+    if int(t.status[0]) == RAY_UNDEFINED:
+        raise RuntimeError("the reference analyzer never returns on this ray (edge-crossing spin)")
+    if int(t.status[0]) == RAY_INVALID:
+        raise ValueError("invalid ray")
+    return t.events, int(t.counters[0, 0]), int(t.counters[0, 1])
+
+
+def query(grid, ijk) -> np.ndarray:
+    """SparseGrid::query (sparse.hpp:163-171) / DenseGrid::voxel_at for points int32 [n, 3]
+    -> QUERY_DTYPE records (occupied, level, origin, extent)."""
+    p = np.ascontiguousarray(np.asarray(ijk, np.int32).reshape(-1, 3))
+    out = np.zeros(p.shape[0], QUERY_DTYPE)
+    _check(lib.sogk_grid_query_host(grid._h, _ptr(p), p.shape[0], out.ctypes.data), "query")
+    return out
 
 
 def release_workspaces():

@@ -1285,6 +1285,132 @@ int sogk_sample_write_camera(sogk_sampler* s, const sogk_camera* cam, int64_t fi
                       d_t_ends, d_ray_indices, d_cells, d_levels, stream);
 }
 
+// ---- traverse ----------------------------------------------------------------
+int sogk_traverse_count(sogk_sampler* s, const double* d_rays, int64_t n, int64_t* d_event_info,
+                        int64_t* d_stats, uint8_t* d_status, int32_t* d_counters, void* stream) {
+    if (!s) return fail(SOGK_INVALID_ARG, "sampler is NULL");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (!d_stats) return fail(SOGK_INVALID_ARG, "stats buffer is NULL");
+    if (n > 0 && (!d_rays || !d_event_info)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    int st = s->wait_levels(stream);
+    if (st) return st;
+    CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
+    if (n == 0) return SOGK_OK;
+    CK(launch_traverse_count(s->v, s->dev, d_rays, n, d_event_info, d_stats, d_status, d_counters,
+                             S(stream)),
+       "traverse launch");
+    // the scan's look-back tiles come from the stream-ordered pool (not the sampling workspace,
+    // whose slabs a pending write may still need)
+    const int64_t tiles = scan_tiles(n);
+    uint64_t* t = nullptr;
+    CK(retain_pool(), "pool");
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&t), size_t(tiles + 2) * 8, S(stream)), "scan tiles");
+    cudaError_t e = cudaMemsetAsync(t, 0, size_t(tiles + 2) * 8, S(stream));
+    if (e == cudaSuccess)
+        e = launch_scan(n, d_event_info, d_stats, t, reinterpret_cast<unsigned int*>(t + tiles), S(stream));
+    cudaFreeAsync(t, S(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "traverse scan");
+    return SOGK_OK;
+}
+
+int sogk_traverse_write(sogk_sampler* s, const double* d_rays, int64_t n,
+                        const int64_t* d_event_info, sogk_event* d_events, void* stream) {
+    if (!s) return fail(SOGK_INVALID_ARG, "sampler is NULL");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
+    if (n == 0) return SOGK_OK;
+    if (!d_rays || !d_event_info || !d_events) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    int st = s->wait_levels(stream);
+    if (st) return st;
+    CK(launch_traverse_write(s->v, s->dev, d_rays, n, d_event_info, d_events, S(stream)), "traverse launch");
+    return SOGK_OK;
+}
+
+int sogk_traverse_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t capacity,
+                       int64_t* h_event_info, sogk_event* h_events, uint8_t* h_status,
+                       int32_t* h_counters, int64_t* h_stats, void* stream) {
+    if (!s || !h_stats) return fail(SOGK_INVALID_ARG, "NULL argument");
+    if (n < 0 || capacity < 0) return fail(SOGK_INVALID_ARG, "negative size");
+    if (n > 0 && (!h_rays || !h_event_info)) return fail(SOGK_INVALID_ARG, "NULL host buffer");
+    std::lock_guard<std::mutex> hold(s->host_mu);
+    for (int k = 0; k < SOGK_STATS_LEN; ++k) h_stats[k] = 0;
+    if (n == 0) return SOGK_OK;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t b_rays = al(size_t(n) * 64), b_info = al(size_t(n) * 16), b_stats = 256,
+                 b_status = al(size_t(n)), b_ctr = al(size_t(n) * 8);
+    char* p = nullptr;
+    CK(cudaMalloc(&p, b_rays + b_info + b_stats + b_status + b_ctr), "traverse scratch");
+    double* d_rays = reinterpret_cast<double*>(p);
+    int64_t* d_info = reinterpret_cast<int64_t*>(p + b_rays);
+    int64_t* d_stats = reinterpret_cast<int64_t*>(p + b_rays + b_info);
+    uint8_t* d_status = reinterpret_cast<uint8_t*>(p + b_rays + b_info + b_stats);
+    int32_t* d_ctr = reinterpret_cast<int32_t*>(p + b_rays + b_info + b_stats + b_status);
+    sogk_event* d_ev = nullptr;
+    int rc = SOGK_OK;
+    cudaError_t e = cudaMemcpyAsync(d_rays, h_rays, size_t(n) * 64, cudaMemcpyHostToDevice, S(stream));
+    if (e == cudaSuccess) {
+        rc = sogk_traverse_count(s, d_rays, n, d_info, d_stats, d_status, d_ctr, stream);
+        if (rc == SOGK_OK) {
+            e = cudaMemcpyAsync(h_stats, d_stats, SOGK_STATS_LEN * 8, cudaMemcpyDeviceToHost, S(stream));
+            if (e == cudaSuccess) e = cudaMemcpyAsync(h_event_info, d_info, size_t(n) * 16, cudaMemcpyDeviceToHost, S(stream));
+            if (e == cudaSuccess && h_status) e = cudaMemcpyAsync(h_status, d_status, size_t(n), cudaMemcpyDeviceToHost, S(stream));
+            if (e == cudaSuccess && h_counters) e = cudaMemcpyAsync(h_counters, d_ctr, size_t(n) * 8, cudaMemcpyDeviceToHost, S(stream));
+            if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+            const int64_t total = h_stats[SOGK_STAT_TOTAL_SAMPLES];
+            if (e == cudaSuccess && total > capacity) {
+                rc = fail(SOGK_INSUFFICIENT_CAPACITY, "event capacity below the event total");
+            } else if (e == cudaSuccess && total > 0) {
+                if (!h_events) {
+                    rc = fail(SOGK_INVALID_ARG, "NULL host event buffer");
+                } else {
+                    e = cudaMalloc(&d_ev, size_t(total) * sizeof(sogk_event));
+                    if (e == cudaSuccess) {
+                        rc = sogk_traverse_write(s, d_rays, n, d_info, d_ev, stream);
+                        if (rc == SOGK_OK)
+                            e = cudaMemcpyAsync(h_events, d_ev, size_t(total) * sizeof(sogk_event),
+                                                cudaMemcpyDeviceToHost, S(stream));
+                        if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+                    }
+                }
+            }
+        }
+    }
+    cudaFree(d_ev);
+    cudaFree(p);
+    if (e != cudaSuccess) return cuda_fail(e, "traverse host path");
+    return rc;
+}
+
+int sogk_grid_query(const sogk_grid* g, const int32_t* d_ijk, int64_t n, sogk_query* d_out,
+                    void* stream) {
+    if (!g) return fail(SOGK_INVALID_ARG, "grid is NULL");
+    if (g->kind == SOGK_GRID_DISTANCE) return fail(SOGK_INVALID_ARG, "query needs a dense or VDB grid");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative point count");
+    if (n == 0) return SOGK_OK;
+    if (!d_ijk || !d_out) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    if (g->ready) CK(cudaStreamWaitEvent(S(stream), g->ready, 0), "grid build wait");
+    CK(launch_query(g->dev(), g->kind == SOGK_GRID_VDB ? 1 : 0, d_ijk, n, d_out, S(stream)), "query launch");
+    return SOGK_OK;
+}
+
+int sogk_grid_query_host(const sogk_grid* g, const int32_t* h_ijk, int64_t n, sogk_query* h_out) {
+    if (!g) return fail(SOGK_INVALID_ARG, "grid is NULL");
+    if (n < 0) return fail(SOGK_INVALID_ARG, "negative point count");
+    if (n == 0) return SOGK_OK;
+    if (!h_ijk || !h_out) return fail(SOGK_INVALID_ARG, "NULL host buffer");
+    char* p = nullptr;
+    const size_t b_in = (size_t(n) * 12 + 255) & ~size_t(255);
+    CK(cudaMalloc(&p, b_in + size_t(n) * sizeof(sogk_query)), "query scratch");
+    cudaError_t e = cudaMemcpy(p, h_ijk, size_t(n) * 12, cudaMemcpyHostToDevice);
+    int rc = SOGK_OK;
+    if (e == cudaSuccess) rc = sogk_grid_query(g, reinterpret_cast<int32_t*>(p), n,
+                                               reinterpret_cast<sogk_query*>(p + b_in), nullptr);
+    if (e == cudaSuccess && rc == SOGK_OK)
+        e = cudaMemcpy(h_out, p + b_in, size_t(n) * sizeof(sogk_query), cudaMemcpyDeviceToHost);
+    cudaFree(p);
+    if (e != cudaSuccess) return cuda_fail(e, "query");
+    return rc;
+}
+
 // ---- compositing consumer ------------------------------------------------
 struct sogk_scene {
     SceneDev dev{};

@@ -82,6 +82,16 @@ cudaError_t launch_shade_accumulate(const Variant& v, const SamplerDev& s, const
                                     double* result, uint8_t* rgb8, cudaStream_t st);
 
 
+// traverse (sogk_traverse.cu): event counts per ray -> info[r] = {0, count}, stats, status,
+// counters [n][2]; then events at the scanned offsets
+cudaError_t launch_traverse_count(const Variant& v, const SamplerDev& s, const double* rays, int64_t n,
+                                  int64_t* info, int64_t* stats, uint8_t* status, int32_t* counters,
+                                  cudaStream_t st);
+cudaError_t launch_traverse_write(const Variant& v, const SamplerDev& s, const double* rays, int64_t n,
+                                  const int64_t* info, sogk_event* events, cudaStream_t st);
+cudaError_t launch_query(const GridDev& g, int vdb, const int32_t* ijk, int64_t n, sogk_query* out,
+                         cudaStream_t st);
+
 // packed_info[r].offset += base for r < n
 cudaError_t launch_add_offset(int64_t* packed, int64_t n, int64_t base, cudaStream_t st);
 

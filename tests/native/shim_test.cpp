@@ -4,6 +4,7 @@
 // compiles the reference headers, so it is test infrastructure); run by
 // tests/test_gpu_shim.py on the GPU box.  Exit 0 = bit-exact everywhere.
 #include <cstdio>
+#include <sstream>
 #include <vector>
 
 #include "sog/sog.hpp"
@@ -117,6 +118,59 @@ int main() {
         EXPECT(g.lookups == ref.lookups && g.steps == ref.steps && g.samples == ref.samples,
                "frame counters differ");
     }
+    // traverse: collect_events + dump_trace (traversal.hpp:339-357) for every analyzer, and
+    // SparseGrid::query
+    {
+        auto dump = [](const std::vector<TraversalEvent>& ev) {
+            std::ostringstream os;
+            dump_trace(os, ev);
+            return os.str();
+        };
+        const gpu::EventStreams ed = gpu::Traverser(ddense).traverse_rays(rays);
+        const gpu::EventStreams eh = gpu::Traverser(dvdb).traverse_rays(rays);
+        const gpu::EventStreams ec = gpu::Traverser(ddist).traverse_rays(rays);
+        long tm = 0;
+        for (std::size_t r = 0; r < rays.size(); ++r) {
+            DdaTraversal a(dense, rays[r]);
+            HddaTraversal b(sparse, rays[r]);
+            CdTraversal c(dist, rays[r]);
+            const auto ea = collect_events(a), eb = collect_events(b), ecd = collect_events(c);
+            tm += dump(ed.ray_events(r)) != dump(ea) || ed.lookup_count(r) != a.lookup_count() ||
+                  ed.step_count(r) != a.step_count();
+            tm += dump(eh.ray_events(r)) != dump(eb) || eh.lookup_count(r) != b.lookup_count() ||
+                  eh.step_count(r) != b.step_count();
+            tm += dump(ec.ray_events(r)) != dump(ecd) || ec.lookup_count(r) != c.lookup_count() ||
+                  ec.step_count(r) != c.step_count();
+        }
+        EXPECT(tm == 0, "%ld event-stream (dump_trace) mismatches", tm);
+        const gpu::EventStreams es = gpu::Traverser(gl).traverse_rays(rays);
+        long cmx = 0;
+        for (std::size_t r = 0; r < rays.size(); ++r) {
+            CascadeTraversal<SparseGrid> ct(sc, rays[r]);
+            std::vector<CascadeEvent> ref; // collect_events slices to TraversalEvent: drain by hand
+            while (auto ev = ct.next()) ref.push_back(*ev);
+            const auto got = es.ray_cascade_events(r);
+            bool same = ref.size() == got.size();
+            for (std::size_t k = 0; same && k < ref.size(); ++k)
+                same = ref[k].ijk == got[k].ijk && ref[k].level == got[k].level && ref[k].t0 == got[k].t0 &&
+                       ref[k].t1 == got[k].t1 && ref[k].occupied == got[k].occupied &&
+                       ref[k].grid_level == got[k].grid_level;
+            cmx += !same || es.lookup_count(r) != ct.lookup_count() || es.step_count(r) != ct.step_count();
+        }
+        EXPECT(cmx == 0, "%ld cascade event-stream mismatches", cmx);
+        EXPECT(dump(gpu::Traverser(ddense).collect_events(rays[777])) ==
+                   dump(collect_events(DdaTraversal(dense, rays[777]))), "single-ray collect_events");
+        long qm = 0;
+        for (int z = -70; z < 140; z += 7)
+            for (int y = -9; y < 80; y += 5)
+                for (int x = -130; x < 200; x += 11) {
+                    const QueryResult a = sparse.query({x, y, z});
+                    const QueryResult b = gpu::query(dvdb, {x, y, z});
+                    qm += a.occupied != b.occupied || a.level != b.level || !(a.origin == b.origin) ||
+                          a.extent != b.extent;
+                }
+        EXPECT(qm == 0, "%ld query mismatches", qm);
+    }
     // errors like the reference
     bool threw = false;
     try {
@@ -125,7 +179,7 @@ int main() {
         threw = true;
     }
     EXPECT(threw, "negative step did not throw std::invalid_argument");
-    std::printf("%s: %zu rays x 4 variants x 2 schedules + cascade + CD + render, %d failures\n",
+    std::printf("%s: %zu rays x 4 variants x 2 schedules + cascade + CD + render + traverse/query, %d failures\n",
                 failures ? "FAILED" : "OK", rays.size(), failures);
     return failures ? 1 : 0;
 }
