@@ -290,6 +290,21 @@ class Workload:
 
             out.copy_(torch.from_numpy(np.ascontiguousarray(self.host_rays(spec))))
 
+    # product-side helpers for the measurement tools (tools/prof_step.py, issue_probe.py)
+    def dense_levels(self, P, obj: int):
+        return [P.DenseGrid(P.GridTransform(r, w, v), b) for r, w, v, b in self.objects[obj]["levels"]]
+
+    def step_schedule(self, P):
+        return P.StepSchedule(*self.schedule)
+
+    def device_rays(self, P, step: int, obj: int, rank: int = 0, world: int = 1):
+        import torch
+
+        spec = self.shard(step, obj, rank, world)
+        out = torch.empty((spec["count"], 8), dtype=torch.float64, device="cuda")
+        self.fill_rays(P, out, spec)
+        return out
+
     def camera(self, P, spec: dict):
         return P.Camera(spec["pos"], (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, self.width, self.height)
 

@@ -447,6 +447,13 @@ __global__ void __launch_bounds__(kWriteBlock)
 // runs, whose samples are adjacent in the output.  Samples past a ray's slab are
 // tail_kernel's.
 constexpr int kGather = 256;
+#ifndef SOGK_GATHER_STAGED
+#define SOGK_GATHER_STAGED 1 // pass-2 output staged in shared memory, stored coalesced
+#endif
+#ifndef SOGK_STAGE_W
+#define SOGK_STAGE_W 2048 // samples per staging window (17 B each in shared memory)
+#endif
+constexpr int kStageW = SOGK_STAGE_W;
 
 template <int SCH>
 __global__ void __launch_bounds__(kGather)
@@ -496,6 +503,19 @@ __global__ void __launch_bounds__(kGather)
     s_roff[tid] = tid < nrays ? incl - nr : INT_MAX;
     const int total = s_wsum[kGather / 32 - 1];
     __syncthreads();
+#if SOGK_GATHER_STAGED
+    // Output staging: each batch of kGather runs covers one contiguous output span [P0, P1)
+    // (runs are in output order); it is produced window by window into shared memory --
+    // short runs by their own lane, long runs by the whole warp, both clipped to the window --
+    // and every window goes out with fully coalesced stores (a warp writes 32 consecutive
+    // samples of each array).  Positions no run covers (the tails of slab-overflow rays) carry
+    // stale values; tail_kernel, next on the stream, overwrites them.
+    __shared__ double s_t[kStageW];
+    __shared__ int32_t s_ri[kStageW];
+    __shared__ uint32_t s_ce[kStageW];
+    __shared__ uint8_t s_lv[kStageW];
+    __shared__ long long s_span[2];
+#endif
     for (int base = 0; base < total; base += kGather) { // block-uniform trip count
         const int q = base + tid;
         const bool have = q < total;
@@ -522,6 +542,81 @@ __global__ void __launch_bounds__(kGather)
             lv = (uint8_t)(a.sl >> 24);
             ri = (int32_t)(ray_index_base + r0 + j);
         }
+#if SOGK_GATHER_STAGED
+        if (tid == 0) s_span[0] = g0; // the batch's first run starts its span
+        if (have && (q + 1 == total || tid + 1 == kGather)) s_span[1] = g0 + n;
+        __syncthreads();
+        const long long P0 = s_span[0], P1 = s_span[1];
+        for (long long w = P0; w < P1; w += kStageW) { // block-uniform
+            const long long we = (P1 - w < kStageW) ? P1 : w + kStageW;
+            if (n > 0 && n <= kShort && g0 < we && g0 + n > w) {
+                double t = first;
+                for (int k = 0; k < n; ++k) {
+                    const long long g = g0 + k;
+                    if (g >= we) break;
+                    if (g >= w) {
+                        const int p = (int)(g - w);
+                        s_t[p] = t;
+                        s_ri[p] = ri;
+                        s_ce[p] = cell;
+                        s_lv[p] = lv;
+                    }
+                    t = t + ladder_step<SCH>(t, s.dt0, s.growth);
+                }
+            }
+            unsigned lm = __ballot_sync(0xffffffffu, n > kShort && g0 < we && g0 + n > w);
+            while (lm) {
+                const int src = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const double f = __shfl_sync(0xffffffffu, first, src);
+                const long long gb = __shfl_sync(0xffffffffu, g0, src);
+                const int nn = __shfl_sync(0xffffffffu, n, src);
+                const uint32_t ce = __shfl_sync(0xffffffffu, cell, src);
+                const int lvl = __shfl_sync(0xffffffffu, (int)lv, src);
+                const int32_t rr = __shfl_sync(0xffffffffu, ri, src);
+                double t1 = 0.0;
+                int64_t b2 = 0, inc = 0, kfast = 1;
+                if (SCH == 0) { // closed form after two explicit in-binade steps (sogk_ladder.cuh)
+                    t1 = f + s.dt0;
+                    const double t2 = t1 + s.dt0;
+                    const int64_t b0 = dbits(f), b1 = dbits(t1);
+                    b2 = dbits(t2);
+                    inc = b2 - b1;
+                    const int64_t e0 = b0 >> 52;
+                    if (e0 == (b2 >> 52) && e0 != 0 && inc > 0) {
+                        const int64_t end = (e0 + 1) << 52;
+                        kfast = 2 + fix_quotient(end - 1 - b2, inc, (dfrom(end) - t2) * s.inv_dt0);
+                    }
+                }
+                const int ka = (int)(w > gb ? w - gb : 0);
+                const int kb = (int)(gb + nn < we ? nn : we - gb);
+                for (int k = ka + lane; k < kb; k += 32) {
+                    double t;
+                    if (SCH == 0 && k <= kfast)
+                        t = k == 0 ? f : (k == 1 ? t1 : dfrom(b2 + (int64_t)(k - 2) * inc));
+                    else
+                        t = ladder_advance<SCH>(f, k, s.dt0, s.inv_dt0, s.growth, s.t_switch);
+                    const int p = (int)(gb + k - w);
+                    s_t[p] = t;
+                    s_ri[p] = rr;
+                    s_ce[p] = ce;
+                    s_lv[p] = (uint8_t)lvl;
+                }
+            }
+            __syncthreads();
+            const int m = (int)(we - w);
+            for (int p = tid; p < m; p += kGather) { // coalesced: consecutive lanes, consecutive samples
+                const long long g = w + p;
+                const double t = s_t[p];
+                __stcs(o.t_starts + g, t);
+                if (o.t_ends) __stcs(o.t_ends + g, t + ladder_step<SCH>(t, s.dt0, s.growth));
+                if (o.ray_indices) __stcs(o.ray_indices + g, s_ri[p]);
+                if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, s_ce[p]);
+                if (o.levels) o.levels[g] = s_lv[p];
+            }
+            __syncthreads();
+        }
+#else
         if (n <= kShort) { // the common case: a voxel's few points, by its own lane
             double t = first;
             for (int k = 0; k < n; ++k) {
@@ -579,6 +674,7 @@ __global__ void __launch_bounds__(kGather)
                 if (o.levels) o.levels[g] = (uint8_t)lvl;
             }
         }
+#endif
     }
 }
 

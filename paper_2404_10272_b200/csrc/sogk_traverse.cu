@@ -34,9 +34,14 @@ __global__ void __launch_bounds__(kTraverseBlock)
         } else {
             typename PickAn<AN, CASC>::type an;
             an.init(ray, s);
-            long long base = 0;
-            if (WRITE) base = reinterpret_cast<const longlong2*>(info)[r].x;
+            long long base = 0, cap = 0;
+            if (WRITE) { // only the counted events: a ray the count flagged (spin) has none
+                const longlong2 pi = reinterpret_cast<const longlong2*>(info)[r];
+                base = pi.x;
+                cap = pi.y;
+            }
             for (;;) { // collect_events: next() until the stream ends
+                if (WRITE && cnt >= cap) break;
                 Event ev;
                 const int got = an.next(s, ev);
                 if (got == 0) break;

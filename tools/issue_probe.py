@@ -26,15 +26,13 @@ def run(cfg):
     import bench
     import paper_2404_10272_b200 as P
 
-    wl = bench.Workload(P, cfg)
+    wl = bench.Workload(cfg, bench.ProductGen(P))
     n = wl.rays_per_object()
-    rays = torch.empty((n, 8), dtype=torch.float64, device="cuda")
     for obj, o in enumerate(wl.objects):
-        dense = [P.DenseGrid(t, b) for t, b in o["levels"]]
-        grids = [P.build_sparse(d) for d in dense]
-        s = P.Sampler(grids, P.Analyzer.hdda, P.KernelKind.skip, wl.schedule, cascade=wl.cascade,
-                      ray_order=1 if cfg == "cfg4" else 0)
-        wl.fill_rays(rays, STEP, obj, 0, 1)
+        grids = [P.build_sparse(d) for d in wl.dense_levels(P, obj)]
+        s = P.Sampler(grids, P.Analyzer.hdda, P.KernelKind.skip, wl.step_schedule(P), cascade=wl.cascade,
+                      ray_order=wl.ray_order)
+        rays = wl.device_rays(P, STEP, obj)
         for _ in range(2):  # warm launch, then the one that is kept
             s.count(rays)
         torch.cuda.synchronize()

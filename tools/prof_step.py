@@ -14,15 +14,13 @@ import paper_2404_10272_b200 as P  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg1"
 var = sys.argv[2] if len(sys.argv) > 2 else "hdda_skip"
 obj = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-wl = bench.Workload(P, cfg)
+wl = bench.Workload(cfg, bench.ProductGen(P))
 an, kk = {"hdda_skip": (1, 1), "hdda_branch": (1, 0), "dda_branch": (0, 0), "dda_skip": (0, 1)}[var]
 o = wl.objects[obj]
-dense = [P.DenseGrid(t, b) for t, b in o["levels"]]
+dense = wl.dense_levels(P, obj)
 grids = [P.build_sparse(d) for d in dense] if an == 1 else dense
-s = P.Sampler(grids, an, kk, wl.schedule, cascade=wl.cascade)
-n = wl.rays_per_object()
-rays = torch.empty((n, 8), dtype=torch.float64, device="cuda")
-wl.fill_rays(rays, 0, obj, 0, 1)
+s = P.Sampler(grids, an, kk, wl.step_schedule(P), cascade=wl.cascade, ray_order=wl.ray_order)
+rays = wl.device_rays(P, 0, obj)
 for it in range(2):
     packed, stats = s.count(rays)
     tot = int(stats[0].item())

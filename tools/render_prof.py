@@ -9,15 +9,15 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2404_10272_b200 as P  # noqa: E402
 
-wl = bench.Workload(P, "cfg1")
+wl = bench.Workload("cfg1", bench.ProductGen(P))
 o = wl.objects[0]
-kind, seed, count, base = o["scene"]
-scene = P.analytic_scene(kind, base, seed=seed, count=count)
-cam = wl.camera(0, 0, 0, 1)
-dense = [P.DenseGrid(t, b) for t, b in o["levels"]]
+kind, seed, count = o["scene"]
+scene = P.analytic_scene(kind, P.GridTransform(*o["levels"][0][:3]), seed=seed, count=count)
+cam = wl.camera(P, wl.shard(0, 0, 0, 1))
+dense = wl.dense_levels(P, 0)
 for an, k in ((1, 1), (0, 0)):
     grids = [P.build_sparse(d) for d in dense] if an == 1 else dense
-    s = P.Sampler(grids, an, k, wl.schedule)
+    s = P.Sampler(grids, an, k, wl.step_schedule(P))
     for _ in range(3):
         f = P.render_frame(s, scene, cam)
     torch.cuda.synchronize()
