@@ -671,7 +671,10 @@ def run_gpu(args):
         if pool is not None:
             pool.shutdown()
         e2e = dict(full_seconds=e2e_full_s, lean_seconds=e2e_lean_s, h2d=nr * 64 * n_obj, workers=n_workers,
-                   full_d2h=samples0 * 20 / args.steps + nr * 16 * n_obj,
+                   # t_ends / ray_indices are expanded on host threads from the downloaded
+                   # t_starts + packed_info (sogk_sample_host, SOGK_HOST_EXPAND): not on the link
+                   full_d2h=samples0 * (8 if os.environ.get("SOGK_HOST_EXPAND", "1") != "0" else 20) / args.steps
+                   + nr * 16 * n_obj,
                    lean_d2h=samples0 * 8 / args.steps + nr * (16 + 12) * n_obj)
 
     # --- max over ranks
@@ -784,7 +787,9 @@ def run_gpu(args):
         line["e2e"] = {"value": total_rays / e2e["full_seconds"], "unit": "rays/s",
                        "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["full_d2h"]),
                        "api": "sogk_sample_host: pinned host rays in; out the north-star packed intervals "
-                              "(packed_info, t_starts, t_ends, ray_indices)",
+                              "(packed_info, t_starts, t_ends, ray_indices) in host memory; t_starts and "
+                              "packed_info cross PCIe, t_ends = t + step(t) and ray_indices are expanded "
+                              "from them on host threads while later chunks are in flight",
                        "host_threads": e2e["workers"],
                        "lean": {"value": total_rays / e2e["lean_seconds"], "unit": "rays/s",
                                 "d2h_bytes_per_step": int(e2e["lean_d2h"]),

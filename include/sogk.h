@@ -139,6 +139,8 @@ int sogk_abi_version(void);
 const char* sogk_status_string(int status);
 /* copies the calling thread's last error message into buf; returns its full length */
 int sogk_last_error(char* buf, size_t len);
+/* sets the calling thread's last error (status passthrough); for layers built on this ABI */
+int sogk_last_error_set(int status, const char* msg);
 /* number of visible CUDA devices (0 on a CPU-only host) */
 int sogk_device_count(void);
 
@@ -149,6 +151,14 @@ int sogk_grid_create_dense(const sogk_transform* t, const uint8_t* h_bits, size_
 /* same from a device payload (e.g. after an NCCL broadcast); the bytes are copied */
 int sogk_grid_create_dense_device(const sogk_transform* t, const uint8_t* d_bits, size_t nbytes,
                                   void* stream, sogk_grid** out);
+/* Multi-GPU setup: rank `root` broadcasts its grid -- the transform, then the
+ * ceil(N/8)-byte payload -- over the caller's NCCL communicator (`nccl_comm` is an ncclComm_t;
+ * NVLink / NVSwitch on one node) and every rank gets the same dense grid; rays then shard with
+ * no data-path collective.  The root passes t and h_bits, other ranks may pass NULL for both.
+ * Collective: every rank of the communicator calls it.  NCCL is resolved at run time
+ * (libnccl.so.2; a copy the process already loaded is preferred). */
+int sogk_grid_create_dense_broadcast(const sogk_transform* t, const uint8_t* h_bits, size_t nbytes,
+                                     int root, void* nccl_comm, void* stream, sogk_grid** out);
 /* build_sparse (sparse.hpp:333-371) on the GPU: ballot/popc masks + prefix-scan leaf slots */
 int sogk_grid_build_vdb(const sogk_grid* dense, void* stream, sogk_grid** out);
 /* build_distance (distance.hpp:45-103): the chessboard distance field of a dense grid

@@ -49,7 +49,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SOGK_LIB", os.path.join(_HERE, "_lib", "libsogk.so"))
+LIB_PATH = os.environ.get("SOGK_LIB") or os.path.join(_HERE, "_lib", "libsogk.so")
 
 OK, INVALID_ARG, CUDA_ERROR, OOM, INSUFFICIENT_CAPACITY, IO_ERROR, NO_DEVICE = range(7)
 RAY_OK, RAY_INVALID, RAY_UNDEFINED = 0, 1, 2

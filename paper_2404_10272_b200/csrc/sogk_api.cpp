@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sogk.h"
@@ -351,8 +352,10 @@ struct sogk_sampler {
     cudaStream_t lanes[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
     int64_t* h_chunk_stats = nullptr;
+    std::vector<cudaEvent_t> done_ev; // per chunk: its downloads finished (host expansion waits)
 
     ~sogk_sampler() {
+        for (cudaEvent_t e : done_ev) cudaEventDestroy(e);
         cudaFree(hb);
         if (lanes_ready) {
             for (int l = 0; l < 3; ++l) {
@@ -491,6 +494,8 @@ const char* sogk_status_string(int s) {
         default: return "unknown status";
     }
 }
+
+int sogk_last_error_set(int status, const char* msg) { return fail(status, msg ? msg : ""); }
 
 int sogk_last_error(char* buf, size_t len) {
     if (buf && len) {
@@ -1654,6 +1659,24 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         const long v = e ? std::atol(e) : 0;
         return int64_t(v >= 1 && v <= 64 ? v : 8);
     }();
+    // t_ends and ray_indices are functions of t_starts and packed_info (t_end = t + step(t),
+    // sampling.hpp:99,118; ray_indices = ray_index_base + r over each ray's range): when the
+    // caller also takes t_starts they are expanded on host threads from the downloaded
+    // t_starts / packed_info of each finished chunk, while the next chunks are on the GPU and
+    // the PCIe link -- the device->host link is the bound of this call, and this cuts its bytes
+    // per sample from 20 to 8.  Same IEEE operation (one add, no FMA), so the bytes are
+    // identical to the device's.  SOGK_HOST_EXPAND=0: download them instead.
+    static const bool kExpand = [] {
+        const char* e = std::getenv("SOGK_HOST_EXPAND");
+        return !(e && e[0] == '0');
+    }();
+    static const int kExpandThreads = [] {
+        const char* e = std::getenv("SOGK_HOST_THREADS");
+        const long v = e ? std::atol(e) : 0;
+        const int hw = int(std::thread::hardware_concurrency());
+        return int(v >= 1 && v <= 64 ? v : std::max(1, std::min(8, hw / 2)));
+    }();
+    const bool expand = kExpand && h_t_starts && (h_t_ends || h_ray_indices);
     // n / 8 rays per chunk, at most 512 K: big calls get a deeper pipeline (shorter fill and
     // drain; 2^24 probe rays: 32 chunks, +4.5 % e2e over 8)
     const int64_t chunk = std::max<int64_t>(65536, std::min<int64_t>((n + kChunks - 1) / kChunks, 1 << 19));
@@ -1662,8 +1685,8 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     const size_t b_rays = al(size_t(n) * 64), b_packed = al(size_t(n) * 16),
                  b_stats = al(size_t(std::max<int64_t>(nchunks, 1)) * SOGK_STATS_LEN * 8),
                  b_status = al(size_t(n)), b_ctr = al(size_t(n) * 12);
-    const size_t b_ts = al(size_t(capacity) * 8), b_te = al(size_t(capacity) * 8),
-                 b_ri = al(size_t(capacity) * 4), b_ce = al(size_t(capacity) * 4),
+    const size_t b_ts = al(size_t(capacity) * 8), b_te = expand ? 0 : al(size_t(capacity) * 8),
+                 b_ri = expand ? 0 : al(size_t(capacity) * 4), b_ce = al(size_t(capacity) * 4),
                  b_lv = al(size_t(capacity));
     const size_t need = b_rays + b_packed + b_stats + b_status + b_ctr + b_ts + b_te + b_ri + b_ce + b_lv;
     if (need > s->hb_bytes) {
@@ -1680,6 +1703,11 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         }
         CK(cudaMallocHost(&s->h_chunk_stats, 64 * SOGK_STATS_LEN * 8), "pinned stats");
         s->lanes_ready = true;
+    }
+    while (int64_t(s->done_ev.size()) < nchunks) {
+        cudaEvent_t e = nullptr;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        s->done_ev.push_back(e);
     }
     char* p = static_cast<char*>(s->hb);
     double* d_rays = reinterpret_cast<double*>(p);
@@ -1710,9 +1738,57 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     for (int k = 0; k < SOGK_STATS_LEN; ++k) h_stats[k] = 0;
     std::vector<int64_t> chunk_stats(size_t(nchunks) * SOGK_STATS_LEN, 0);
     std::vector<uint64_t> tokens(size_t(nchunks), 0);
+    std::vector<int64_t> chunk_base(size_t(nchunks), -1); // output offset of a written chunk
     int64_t base = 0;
     bool fits = true;
     int rc = SOGK_OK;
+    // host expansion of t_ends / ray_indices, chunk by chunk as their downloads finish
+    const double dt0 = s->dev.dt0, growth = s->dev.growth;
+    const bool linear = s->v.linear != 0;
+    std::atomic<int64_t> issued{0};   // chunks whose write + downloads are issued
+    std::atomic<bool> abort_exp{false};
+    auto expand_chunk = [&](int64_t c) {
+        const int64_t r0 = c * chunk, m = std::min(chunk, n - r0);
+        auto work = [&](int64_t a, int64_t b) { // rays [a, b) of the chunk
+            for (int64_t r = r0 + a; r < r0 + b; ++r) {
+                const int64_t off = h_packed_info[2 * r], cnt = h_packed_info[2 * r + 1];
+                if (h_ray_indices) {
+                    const int32_t ri = int32_t(ray_index_base + r);
+                    for (int64_t k = 0; k < cnt; ++k) h_ray_indices[off + k] = ri;
+                }
+                if (h_t_ends) {
+                    if (linear) {
+                        for (int64_t k = 0; k < cnt; ++k) {
+                            const double t = h_t_starts[off + k], g = growth * t;
+                            h_t_ends[off + k] = t + ((dt0 < g) ? g : dt0); // std::max(dt0, growth * t)
+                        }
+                    } else {
+                        for (int64_t k = 0; k < cnt; ++k) h_t_ends[off + k] = h_t_starts[off + k] + dt0;
+                    }
+                }
+            }
+        };
+        const int T = int(std::min<int64_t>(kExpandThreads, std::max<int64_t>(1, m / 4096)));
+        if (T <= 1) {
+            work(0, m);
+            return;
+        }
+        std::vector<std::thread> th;
+        for (int i = 1; i < T; ++i) th.emplace_back(work, m * i / T, m * (i + 1) / T);
+        work(0, m / T);
+        for (auto& x : th) x.join();
+    };
+    std::thread expander;
+    if (expand && nchunks > 0) {
+        expander = std::thread([&] {
+            for (int64_t c = 0; c < nchunks; ++c) {
+                while (issued.load() <= c && !abort_exp.load()) std::this_thread::yield();
+                if (abort_exp.load()) return;
+                if (cudaEventSynchronize(s->done_ev[c]) != cudaSuccess) return;
+                if (chunk_base[size_t(c)] >= 0) expand_chunk(c);
+            }
+        });
+    }
     // pass 1 of chunk c (upload, count, scan, stats download) on lane c % kLanes
     auto issue_count = [&](int64_t c) -> int {
         cudaStream_t L = s->lanes[c % kLanes];
@@ -1737,16 +1813,18 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         const int64_t tot = hs[SOGK_STAT_TOTAL_SAMPLES];
         CK(launch_add_offset(d_packed + 2 * r0, m, base, L), "offsets");
         if (fits && base + tot <= capacity) {
+            chunk_base[size_t(c)] = base;
             if (tot > 0) {
                 const int st = write_impl(s, d_rays + 8 * r0, nullptr, 0, m, d_packed + 2 * r0,
-                                          tokens[size_t(c)], ray_index_base + r0, d_ts, h_t_ends ? d_te : nullptr,
-                                          h_ray_indices ? d_ri : nullptr, h_cells ? d_ce : nullptr,
+                                          tokens[size_t(c)], ray_index_base + r0, d_ts,
+                                          (h_t_ends && !expand) ? d_te : nullptr,
+                                          (h_ray_indices && !expand) ? d_ri : nullptr, h_cells ? d_ce : nullptr,
                                           h_levels ? d_lv : nullptr, L);
                 if (st) return st;
                 const size_t o = size_t(base), tb = size_t(tot);
                 if (h_t_starts) CK(cudaMemcpyAsync(h_t_starts + o, d_ts + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
-                if (h_t_ends) CK(cudaMemcpyAsync(h_t_ends + o, d_te + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
-                if (h_ray_indices) CK(cudaMemcpyAsync(h_ray_indices + o, d_ri + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_t_ends && !expand) CK(cudaMemcpyAsync(h_t_ends + o, d_te + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_ray_indices && !expand) CK(cudaMemcpyAsync(h_ray_indices + o, d_ri + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
                 if (h_cells) CK(cudaMemcpyAsync(h_cells + o, d_ce + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
                 if (h_levels) CK(cudaMemcpyAsync(h_levels + o, d_lv + o, tb, cudaMemcpyDeviceToHost, L), "D2H");
             }
@@ -1756,6 +1834,8 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         CK(cudaMemcpyAsync(h_packed_info + 2 * r0, d_packed + 2 * r0, size_t(m) * 16, cudaMemcpyDeviceToHost, L), "D2H");
         if (h_status) CK(cudaMemcpyAsync(h_status + r0, d_status + r0, size_t(m), cudaMemcpyDeviceToHost, L), "D2H");
         if (h_counters) CK(cudaMemcpyAsync(h_counters + 3 * r0, d_ctr + 3 * r0, size_t(m) * 12, cudaMemcpyDeviceToHost, L), "D2H");
+        CK(cudaEventRecord(s->done_ev[c], L), "event");
+        issued.store(c + 1);
         base += tot;
         return SOGK_OK;
     };
@@ -1764,7 +1844,12 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         if (rc == SOGK_OK && c > 0) rc = issue_write(c - 1);
         if (c + 1 == nchunks && rc == SOGK_OK) rc = issue_write(c);
     }
-    for (int l = 0; l < kLanes; ++l) CK(cudaStreamSynchronize(s->lanes[l]), "pipeline sync");
+    if (rc != SOGK_OK) abort_exp.store(true);
+    for (int l = 0; l < kLanes; ++l) {
+        const cudaError_t e = cudaStreamSynchronize(s->lanes[l]);
+        if (e != cudaSuccess && rc == SOGK_OK) rc = cuda_fail(e, "pipeline sync");
+    }
+    if (expander.joinable()) expander.join();
     if (rc) return rc;
     for (int64_t c = 0; c < nchunks; ++c)
         for (int k = 0; k < SOGK_STATS_LEN; ++k) {

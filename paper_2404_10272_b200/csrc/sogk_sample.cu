@@ -455,8 +455,11 @@ constexpr int kGather = 256;
 #endif
 constexpr int kStageW = SOGK_STAGE_W;
 
+#ifndef SOGK_GATHER_MINB
+#define SOGK_GATHER_MINB 1
+#endif
 template <int SCH>
-__global__ void __launch_bounds__(kGather)
+__global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
     gather_kernel(const __grid_constant__ SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
                   const SlabDev S, int64_t ray_index_base, const Out o) {
     __shared__ int s_roff[kGather + 1]; // local run offsets (exclusive), INT_MAX past the rays
@@ -516,6 +519,23 @@ __global__ void __launch_bounds__(kGather)
     __shared__ uint8_t s_lv[kStageW];
     __shared__ long long s_span[2];
 #endif
+    // run records of the next batch are loaded while the current one is expanded (software
+    // pipelining: the scattered 16-byte record loads are the kernel's long-scoreboard stall)
+    auto locate = [&](int q, int& j) -> const RunRec* {
+        j = 0; // largest j with s_roff[j] <= q: branch-free binary search
+#pragma unroll
+        for (int step = kGather / 2; step > 0; step >>= 1)
+            j += (s_roff[j + step] <= q) ? step : 0;
+        return S.runs + (r0 + j) * S.C + (q - s_roff[j]);
+    };
+    RunRec pa{};
+    uint32_t pnsl = 0xffffffffu; // next record's start | level, or ~0: the ray's fill ends the run
+    int pj = 0;
+    if (tid < total) {
+        const RunRec* rec = locate(tid, pj);
+        pa = *rec;
+        if (tid - s_roff[pj] + 1 < s_nr[pj]) pnsl = rec[1].sl;
+    }
     for (int base = 0; base < total; base += kGather) { // block-uniform trip count
         const int q = base + tid;
         const bool have = q < total;
@@ -526,21 +546,19 @@ __global__ void __launch_bounds__(kGather)
         uint8_t lv = 0;
         int32_t ri = 0;
         if (have) {
-            int j = 0; // largest j with s_roff[j] <= q: branch-free binary search
-#pragma unroll
-            for (int step = kGather / 2; step > 0; step >>= 1)
-                j += (s_roff[j + step] <= q) ? step : 0;
-            const int local = q - s_roff[j];
-            const RunRec* rec = S.runs + (r0 + j) * S.C + local;
-            const RunRec a = *rec;
-            const int start = (int)(a.sl & kRunStartMax);
-            const int end = local + 1 < s_nr[j] ? (int)(rec[1].sl & kRunStartMax) : s_fill[j];
-            first = a.first;
-            g0 = s_off[j] + start;
+            const int start = (int)(pa.sl & kRunStartMax);
+            const int end = pnsl != 0xffffffffu ? (int)(pnsl & kRunStartMax) : s_fill[pj];
+            first = pa.first;
+            g0 = s_off[pj] + start;
             n = end - start;
-            cell = a.cell;
-            lv = (uint8_t)(a.sl >> 24);
-            ri = (int32_t)(ray_index_base + r0 + j);
+            cell = pa.cell;
+            lv = (uint8_t)(pa.sl >> 24);
+            ri = (int32_t)(ray_index_base + r0 + pj);
+        }
+        if (q + kGather < total) { // prefetch the next batch's record
+            const RunRec* rec = locate(q + kGather, pj);
+            pa = *rec;
+            pnsl = (q + kGather - s_roff[pj] + 1 < s_nr[pj]) ? rec[1].sl : 0xffffffffu;
         }
 #if SOGK_GATHER_STAGED
         if (tid == 0) s_span[0] = g0; // the batch's first run starts its span
