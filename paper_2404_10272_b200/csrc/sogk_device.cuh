@@ -376,6 +376,9 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
 #ifndef SOGK_HDDA_SMEM
 #define SOGK_HDDA_SMEM 1
 #endif
+#ifndef SOGK_VOXEL_FAST
+#define SOGK_VOXEL_FAST 1 // incremental exact stepping through voxel-level nodes (NodeAn::next)
+#endif
 // Kernels using the node analyzers or the cascade launch 1-D blocks of at most kGeomBlock
 // threads (per-thread shared-memory columns).
 constexpr int kGeomBlock = 128;
@@ -385,6 +388,8 @@ constexpr int kGeomBlock = 128;
 struct HddaGeomSmem {
     double e[3][kGeomBlock], dv[3][kGeomBlock], iv[3][kGeomBlock];
     double te[kGeomBlock], tx[kGeomBlock];
+    double mg[3][kGeomBlock]; // voxel fast path: re-derivation safety margin per axis (time)
+    double tp[3][kGeomBlock]; // voxel fast path: crossing time of the axis's last stepped plane
     int m[3][kGeomBlock];
 };
 __device__ __forceinline__ HddaGeomSmem& hdda_geom() {
@@ -405,6 +410,8 @@ struct NodeAn {
     __device__ __forceinline__ double& DV(int a) { return hdda_geom().dv[a][threadIdx.x]; }
     __device__ __forceinline__ double& IV(int a) { return hdda_geom().iv[a][threadIdx.x]; }
     __device__ __forceinline__ int& M(int a) { return hdda_geom().m[a][threadIdx.x]; }
+    __device__ __forceinline__ double& MG(int a) { return hdda_geom().mg[a][threadIdx.x]; }
+    __device__ __forceinline__ double& TP(int a) { return hdda_geom().tp[a][threadIdx.x]; }
     __device__ __forceinline__ double& TE() { return hdda_geom().te[threadIdx.x]; }
     __device__ __forceinline__ double& TX() { return hdda_geom().tx[threadIdx.x]; }
     __device__ __forceinline__ double TE() const { return hdda_geom().te[threadIdx.x]; }
@@ -413,6 +420,9 @@ struct NodeAn {
     double e[3], dv[3], iv[3]; // mirrored entry, |dir|, 1/|dir|
     int m[3];                  // -1 on mirrored axes, else 0
     double t_enter, t_exit;
+    double mg[3], tp[3];
+    __device__ __forceinline__ double& MG(int a) { return mg[a]; }
+    __device__ __forceinline__ double& TP(int a) { return tp[a]; }
     __device__ __forceinline__ double& E(int a) { return e[a]; }
     __device__ __forceinline__ double& DV(int a) { return dv[a]; }
     __device__ __forceinline__ double& IV(int a) { return iv[a]; }
@@ -431,12 +441,18 @@ struct NodeAn {
     bool done;
     bool undefined;
     VdbCursor cur;
+    // voxel fast path (SOGK_VOXEL_FAST): exit-plane times of the current voxel, kept across
+    // consecutive voxel-level iterations, and per-axis state for the re-derivation proof
+    double tcv[3];
+    unsigned fstate; // bit 0: tcv valid; bit 1: state known (fast path allowed); bits 2..4:
+                     // axis a's lower bound still to be proven (its cell came from a step)
 
     __device__ __forceinline__ void init(const Ray& r, const GridDev& g, int cap) {
         lookups = steps = 0;
         undefined = false;
         spin_cap = cap;
         degenerate = 0;
+        fstate = 0;
         cur.reset();
         Geom geom;
         geom.init(r, g);
@@ -466,10 +482,35 @@ struct NodeAn {
                 M(a) = 0;
             }
         }
+#if SOGK_VOXEL_FAST
+        // Re-derivation margin (time units), see next(): with u = 2^-53, |grid_coord error| <=
+        // 5.1 u R and |plane_t - exact crossing| <= 1.01 u |t| + 6.1 u R / |dir|, R bounding the
+        // mirrored coordinates; 2^-50 T and 2^-46 R / |dir| cover both with room to spare.
+        const double T = 2.0 * ((geom.t_exit > geom.t_enter) ? geom.t_exit : geom.t_enter) + 1.0;
+        int rmax = g.res[0] > g.res[1] ? g.res[0] : g.res[1];
+        rmax = rmax > g.res[2] ? rmax : g.res[2];
+        const double R = (double)rmax + 2.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            MG(a) = geom.step[a] != 0 ? T * 0x1p-50 + R * 0x1p-46 * fabs(geom.inv[a]) : 0.0;
+#endif
     }
 
     // One iteration of HddaTraversal::next's loop (:213-248): 1 = event, 0 = end,
     // -1 = degenerate iteration consumed (call again).
+    //
+    // Voxel fast path (SOGK_VOXEL_FAST).  Inside mixed leaves every node is a voxel (extent 1),
+    // whose exit plane on each axis depends on that axis's cell only, and a step changes one
+    // axis: the other axes keep their exit-plane times (same inputs, same bits) and their cells
+    // -- unless the reference's re-derivation at t1 (cell_after_crossing, :91-104) lands
+    // elsewhere, which it can only do near a tie.  The re-derived cell of a non-stepped axis
+    // equals the current one when grid_coord(t1) is provably inside [lo, lo + 1): upper side
+    // t1 + MG < (its exit-plane time), lower side t1 > TP + MG for an axis whose cell came from a
+    // step at TP (a cell that came from a re-derivation, or passed this test once, keeps its
+    // lower side: grid_coord is monotone in t, each FP op being monotone).  Then the iteration
+    // is one plane_t for the stepped axis and no re-derivation; anything else -- ties, near-
+    // ties, degenerate crossings, non-voxel nodes, the final event -- takes the exact path.
+    // Events, cells and counters are the reference's bit for bit.
     __device__ __forceinline__ int next(const GridDev& g, Event& ev) {
         if (done) return 0;
         Query q;
@@ -491,11 +532,23 @@ struct NodeAn {
         const double te = TE();
         double tc[3];
         int pl[3];
+#if SOGK_VOXEL_FAST
+        const bool vox = q.ext == 1;
+        const bool cached = vox && (fstate & 1u);
+#else
+        constexpr bool cached = false;
+#endif
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const int lo = CD ? ijk[a] - half : (ijk[a] & -q.ext);
             ev.ijk[a] = lo;
             pl[a] = (lo ^ M(a)) + (M(a) ? 1 : q.ext);
+#if SOGK_VOXEL_FAST
+            if (cached) {
+                tc[a] = tcv[a];
+                continue;
+            }
+#endif
             tc[a] = te + ((double)pl[a] - E(a)) * IV(a);
         }
         double t1;
@@ -511,6 +564,41 @@ struct NodeAn {
             return 1;
         }
         const bool degen = t1 <= t_cur; // degenerate corner crossing (:238-241)
+#if SOGK_VOXEL_FAST
+        if (vox && !degen && (fstate & 2u)) {
+            bool ok = true;
+            unsigned lower = fstate;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (a == axis || DV(a) == 0.0) continue; // stepped or static axis
+                const double mg = MG(a);
+                ok = ok && (t1 + mg < tc[a]);
+                if (lower & (4u << a)) {
+                    ok = ok && (t1 > TP(a) + mg);
+                    lower &= ~(4u << a);
+                }
+            }
+            if (ok) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    if (a != axis) {
+                        tcv[a] = tc[a];
+                        continue;
+                    }
+                    ijk[a] = pl[a] ^ M(a);
+                    tcv[a] = te + ((double)(pl[a] + 1) - E(a)) * IV(a); // the next voxel's plane
+                    TP(a) = t1;
+                }
+                fstate = (lower | 3u) | (4u << axis);
+                degenerate = 0;
+                ev.t0 = t_cur;
+                ev.t1 = t1;
+                ++steps;
+                t_cur = t1;
+                return 1;
+            }
+        }
+#endif
         // cell_after_crossing (:91-104) at t_cur (degenerate) or t1, all axes
         // evaluated and the stepped one overridden
         const double dt = (degen ? t_cur : t1) - te;
@@ -519,6 +607,12 @@ struct NodeAn {
             const int c = __double2int_rd(E(a) + dt * DV(a)) ^ M(a);
             ijk[a] = (a == axis) ? (pl[a] ^ M(a)) : c;
         }
+#if SOGK_VOXEL_FAST
+        // every cell is now a re-derivation at t1 (or t_cur) except the stepped axis's, set at
+        // its crossing time t1
+        TP(axis) = t1;
+        fstate = 2u | (4u << axis);
+#endif
         if (degen) {
             // the reference spins forever at exact edge crossings
             if (++degenerate > spin_cap) {
@@ -546,6 +640,7 @@ struct NodeAn {
     __device__ __forceinline__ void restore(const GridDev&, const int in_ijk[3], double in_t) {
         done = false;
         degenerate = 0;
+        fstate = 0; // the first iteration after a resume is exact
         t_cur = in_t;
         ijk[0] = in_ijk[0];
         ijk[1] = in_ijk[1];

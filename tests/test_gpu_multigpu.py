@@ -24,4 +24,4 @@ def test_nccl_broadcast_helper(tmp_path):
     env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0])
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.startswith("OK"), out.stdout
+    assert "\nOK:" in "\n" + out.stdout, out.stdout
