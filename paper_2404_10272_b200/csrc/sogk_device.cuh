@@ -379,6 +379,9 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
 #ifndef SOGK_VOXEL_FAST
 #define SOGK_VOXEL_FAST 1 // incremental exact stepping through voxel-level nodes (NodeAn::next)
 #endif
+#ifndef SOGK_VF_CACHE
+#define SOGK_VF_CACHE 1 // keep the voxel exit-plane times across iterations (else recompute)
+#endif
 // Kernels using the node analyzers or the cascade launch 1-D blocks of at most kGeomBlock
 // threads (per-thread shared-memory columns).
 constexpr int kGeomBlock = 128;
@@ -534,7 +537,7 @@ struct NodeAn {
         int pl[3];
 #if SOGK_VOXEL_FAST
         const bool vox = q.ext == 1;
-        const bool cached = vox && (fstate & 1u);
+        const bool cached = SOGK_VF_CACHE && vox && (fstate & 1u);
 #else
         constexpr bool cached = false;
 #endif
@@ -951,8 +954,9 @@ struct RunGen {
     // advanced past ev.t0 (t_last0 = where it stood before) and the caller takes the
     // points t_last <= ev.t1 (sampling.hpp:96-99, 115-118), e.g. with seek_to().
     // The branch kernel's per-point probe (DenseProbe / SparseProbe / CascadeProbe) asks
-    // the grid about ev.ijk, i.e. the event's own cell or node, so it always answers
-    // ev.occ; it is not evaluated, only counted (kernel_lookups += points of the event).
+    // the grid about ev.ijk, i.e. the event's own cell or node, so it answers ev.occ and is
+    // counted, not evaluated (kernel_lookups += points of the event) -- except on HDDA
+    // root-tile events, where it is evaluated once (see step_event).
     __device__ __forceinline__ int step_event(const SamplerDev& s, Event& ev, double& t_last0) {
         if (!(alive && t_last <= t_end)) {
             alive = false;
@@ -965,6 +969,12 @@ struct RunGen {
         }
         if (got < 0) return 1; // analyzer-internal iteration, no event yet
         if (!Branch && !ev.occ) return 1;
+        // The branch kernel's probe (SparseProbe, sampling.hpp:59-67) queries the grid at
+        // ev.ijk.  That is the event's own node -- answer ev.occ -- except for an HDDA root-tile
+        // event (a cell just outside the grid, e.g. the sliver before t_exit when the
+        // re-derived cell has left the box): its ijk is the region origin, which can be an
+        // in-bounds voxel, and the reference samples there if that voxel is occupied.
+        if (Branch && ev.level == LV_ROOT_TILE && !ev.occ) ev.occ = an.probe(s, ev);
         t_last0 = t_last;
         ladder_seek<Sched>(t_last, ev.t0, s.dt0, s.inv_dt0, s.growth, s.t_switch, stalled);
         if (!ev.occ) { // branch kernel, empty event: its points are probed, not sampled

@@ -55,7 +55,6 @@ struct SamplerDev {
     int spin_cap;
     double dt0, growth;
     double inv_dt0;  // 1/dt0, jump-length estimates only
-    int refill_min;  // persistent kernels: refill when at least this many lanes are idle
     double t_switch; // linear schedule: largest t with fl(growth * t) <= dt0 (DBL_MAX if growth == 0)
 };
 
