@@ -475,35 +475,6 @@ struct sogk_sampler {
 };
 
 // ---------------------------------------------------------------------------
-// host expansion helpers (sogk_sample_host): streaming stores, same IEEE adds as the device
-// ---------------------------------------------------------------------------
-#include <emmintrin.h>
-static void stream_fill_i32(int32_t* dst, int64_t n, int32_t v) {
-    int64_t i = 0;
-    for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) dst[i] = v;
-    const __m128i x = _mm_set1_epi32(v);
-    for (; i + 4 <= n; i += 4) _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), x);
-    for (; i < n; ++i) dst[i] = v;
-}
-static void stream_t_ends_const(const double* ts, double* te, int64_t n, double dt0) {
-    int64_t i = 0;
-    for (; i < n && (reinterpret_cast<uintptr_t>(te + i) & 15); ++i) te[i] = ts[i] + dt0;
-    const __m128d d = _mm_set1_pd(dt0);
-    for (; i + 2 <= n; i += 2) _mm_stream_pd(te + i, _mm_add_pd(_mm_loadu_pd(ts + i), d));
-    for (; i < n; ++i) te[i] = ts[i] + dt0;
-}
-static void stream_t_ends_linear(const double* ts, double* te, int64_t n, double dt0, double growth) {
-    auto step = [&](double t) {
-        const double g = growth * t;
-        return t + ((dt0 < g) ? g : dt0); // std::max(dt0, growth * t), sampling.hpp:36-38
-    };
-    int64_t i = 0;
-    for (; i < n && (reinterpret_cast<uintptr_t>(te + i) & 15); ++i) te[i] = step(ts[i]);
-    for (; i + 2 <= n; i += 2) _mm_stream_pd(te + i, _mm_set_pd(step(ts[i + 1]), step(ts[i])));
-    for (; i < n; ++i) te[i] = step(ts[i]);
-}
-
-// ---------------------------------------------------------------------------
 // library
 // ---------------------------------------------------------------------------
 extern "C" {
@@ -1778,8 +1749,6 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     std::atomic<bool> abort_exp{false};
     auto expand_chunk = [&](int64_t c) {
         const int64_t r0 = c * chunk, m = std::min(chunk, n - r0);
-        // non-temporal (streaming) stores: the outputs are written once and not read back
-        // here, so they bypass the read-for-ownership traffic of ordinary stores
         auto work = [&](int64_t a, int64_t b) { // rays [a, b) of the chunk
             if (a >= b) return;
             const int64_t lo = h_packed_info[2 * (r0 + a)];
@@ -1787,16 +1756,22 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
             if (h_ray_indices) {
                 for (int64_t r = r0 + a; r < r0 + b; ++r) {
                     const int64_t off = h_packed_info[2 * r], cnt = h_packed_info[2 * r + 1];
-                    stream_fill_i32(h_ray_indices + off, cnt, int32_t(ray_index_base + r));
+                    const int32_t ri = int32_t(ray_index_base + r);
+                    for (int64_t k = 0; k < cnt; ++k) h_ray_indices[off + k] = ri;
                 }
             }
             if (h_t_ends) {
-                if (linear)
-                    stream_t_ends_linear(h_t_starts + lo, h_t_ends + lo, hi - lo, dt0, growth);
-                else
-                    stream_t_ends_const(h_t_starts + lo, h_t_ends + lo, hi - lo, dt0);
+                const double* ts = h_t_starts;
+                double* te = h_t_ends;
+                if (linear) {
+                    for (int64_t i = lo; i < hi; ++i) {
+                        const double t = ts[i], g = growth * t;
+                        te[i] = t + ((dt0 < g) ? g : dt0); // std::max(dt0, growth * t)
+                    }
+                } else {
+                    for (int64_t i = lo; i < hi; ++i) te[i] = ts[i] + dt0;
+                }
             }
-            _mm_sfence(); // this thread's streaming stores are globally visible before it ends
         };
         const int T = int(std::min<int64_t>(kExpandThreads, std::max<int64_t>(1, m / 4096)));
         if (T <= 1) {

@@ -393,6 +393,7 @@ struct HddaGeomSmem {
     double te[kGeomBlock], tx[kGeomBlock];
     double mg[3][kGeomBlock]; // voxel fast path: re-derivation safety margin per axis (time)
     double tp[3][kGeomBlock]; // voxel fast path: crossing time of the axis's last stepped plane
+    double tv[3][kGeomBlock]; // voxel fast path: exit-plane times of the current voxel
     int m[3][kGeomBlock];
 };
 __device__ __forceinline__ HddaGeomSmem& hdda_geom() {
@@ -415,6 +416,7 @@ struct NodeAn {
     __device__ __forceinline__ int& M(int a) { return hdda_geom().m[a][threadIdx.x]; }
     __device__ __forceinline__ double& MG(int a) { return hdda_geom().mg[a][threadIdx.x]; }
     __device__ __forceinline__ double& TP(int a) { return hdda_geom().tp[a][threadIdx.x]; }
+    __device__ __forceinline__ double& TV(int a) { return hdda_geom().tv[a][threadIdx.x]; }
     __device__ __forceinline__ double& TE() { return hdda_geom().te[threadIdx.x]; }
     __device__ __forceinline__ double& TX() { return hdda_geom().tx[threadIdx.x]; }
     __device__ __forceinline__ double TE() const { return hdda_geom().te[threadIdx.x]; }
@@ -423,9 +425,10 @@ struct NodeAn {
     double e[3], dv[3], iv[3]; // mirrored entry, |dir|, 1/|dir|
     int m[3];                  // -1 on mirrored axes, else 0
     double t_enter, t_exit;
-    double mg[3], tp[3];
+    double mg[3], tp[3], tv[3];
     __device__ __forceinline__ double& MG(int a) { return mg[a]; }
     __device__ __forceinline__ double& TP(int a) { return tp[a]; }
+    __device__ __forceinline__ double& TV(int a) { return tv[a]; }
     __device__ __forceinline__ double& E(int a) { return e[a]; }
     __device__ __forceinline__ double& DV(int a) { return dv[a]; }
     __device__ __forceinline__ double& IV(int a) { return iv[a]; }
@@ -444,10 +447,9 @@ struct NodeAn {
     bool done;
     bool undefined;
     VdbCursor cur;
-    // voxel fast path (SOGK_VOXEL_FAST): exit-plane times of the current voxel, kept across
-    // consecutive voxel-level iterations, and per-axis state for the re-derivation proof
-    double tcv[3];
-    unsigned fstate; // bit 0: tcv valid; bit 1: state known (fast path allowed); bits 2..4:
+    // voxel fast path (SOGK_VOXEL_FAST): per-axis state for the re-derivation proof (the
+    // current voxel's exit-plane times live in the TV columns)
+    unsigned fstate; // bit 0: TV valid; bit 1: state known (fast path allowed); bits 2..4:
                      // axis a's lower bound still to be proven (its cell came from a step)
 
     __device__ __forceinline__ void init(const Ray& r, const GridDev& g, int cap) {
@@ -536,8 +538,11 @@ struct NodeAn {
         double tc[3];
         int pl[3];
 #if SOGK_VOXEL_FAST
+        // Both fast-path decisions are warp votes: a SIMT warp pays for every path one of its
+        // lanes takes, so the shortcut is taken only when every active lane can take it
+        // (coherent rays through mixed leaves), never as a divergent side path.
         const bool vox = q.ext == 1;
-        const bool cached = SOGK_VF_CACHE && vox && (fstate & 1u);
+        const bool cached = __all_sync(__activemask(), SOGK_VF_CACHE && vox && (fstate & 1u));
 #else
         constexpr bool cached = false;
 #endif
@@ -548,7 +553,7 @@ struct NodeAn {
             pl[a] = (lo ^ M(a)) + (M(a) ? 1 : q.ext);
 #if SOGK_VOXEL_FAST
             if (cached) {
-                tc[a] = tcv[a];
+                tc[a] = TV(a);
                 continue;
             }
 #endif
@@ -568,8 +573,8 @@ struct NodeAn {
         }
         const bool degen = t1 <= t_cur; // degenerate corner crossing (:238-241)
 #if SOGK_VOXEL_FAST
-        if (vox && !degen && (fstate & 2u)) {
-            bool ok = true;
+        {
+            bool ok = vox && !degen && (fstate & 2u);
             unsigned lower = fstate;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -581,15 +586,15 @@ struct NodeAn {
                     lower &= ~(4u << a);
                 }
             }
-            if (ok) {
+            if (__all_sync(__activemask(), ok)) {
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     if (a != axis) {
-                        tcv[a] = tc[a];
+                        TV(a) = tc[a];
                         continue;
                     }
                     ijk[a] = pl[a] ^ M(a);
-                    tcv[a] = te + ((double)(pl[a] + 1) - E(a)) * IV(a); // the next voxel's plane
+                    TV(a) = te + ((double)(pl[a] + 1) - E(a)) * IV(a); // the next voxel's plane
                     TP(a) = t1;
                 }
                 fstate = (lower | 3u) | (4u << axis);

@@ -48,7 +48,11 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out-cap-gb", type=float, default=48.0)
     ap.add_argument("--out", default="gpurun_out/cfg5")
+    ap.add_argument("--fractions", default=",".join(str(f) for f in FRACTIONS))
+    ap.add_argument("--families", default="blocky,random")
     a = ap.parse_args()
+    fracs = [float(x) for x in a.fractions.split(",")]
+    fams = a.families.split(",")
     os.makedirs(a.out, exist_ok=True)
     t = P.GridTransform.cube(a.res, (-1.0, -1.0, -1.0), 2.0)
     sched = P.StepSchedule.constant(0.5 * t.voxel_size)
@@ -57,8 +61,8 @@ def main():
     rays = torch.from_numpy(rays_h).cuda()
     del rays_h
     rows = []
-    for family in ("blocky", "random"):
-        for f in FRACTIONS:
+    for family in fams:
+        for f in fracs:
             bits = (P.random_blocky_grid(t, 7, f, 0.001) if family == "blocky"
                     else P.random_grid(t, 7, f))
             occ = float(np.unpackbits(bits, bitorder="little")[:t.voxel_count()].mean())
@@ -109,8 +113,8 @@ def main():
     # crossover table: HDDA / DDA rays/s per occupancy at each ray count
     lines = ["family,fraction,occupancy,rays,hdda_Mrays_s,dda_Mrays_s,hdda_over_dda,build_ms,hdda_launch_ms"]
     idx = {(r["family"], r["fraction"], r["rays"], r["variant"]): r for r in rows}
-    for family in ("blocky", "random"):
-        for f in FRACTIONS:
+    for family in fams:
+        for f in fracs:
             for lg in range(a.log2_min, a.log2_max + 1):
                 h = idx.get((family, f, 1 << lg, "sparse+hdda+skip"))
                 d = idx.get((family, f, 1 << lg, "dense+dda+branch"))
