@@ -189,6 +189,18 @@ struct Query {
 
 constexpr int kNoLeaf = -(1 << 29); // leaf-cache origin that no coordinate can hit
 
+// dynamic shared memory of the launching kernel (the staged child table when GridDev::smem_tab)
+extern __shared__ int32_t sogk_dyn_smem[];
+
+#ifndef SOGK_QUERY_CACHE
+#define SOGK_QUERY_CACHE 0 // 1: per-thread cached leaf (divergent miss path); 0: uniform walk
+#endif
+
+// child table entry ci of `node` (the root entry of an in-grid region, >= 0)
+__device__ __forceinline__ int32_t table_at(const GridDev& g, int32_t node, int ci) {
+    return g.smem_tab ? sogk_dyn_smem[ci] : __ldg(g.table + (int64_t)node * 4096 + ci);
+}
+
 struct VdbCursor {
     int lo[3];       // cached leaf origin (kNoLeaf: none)
     int64_t leaf;    // cached leaf index
@@ -197,6 +209,7 @@ struct VdbCursor {
 
     __device__ __forceinline__ Query query(const GridDev& g, const int ijk[3]) {
         Query q;
+#if SOGK_QUERY_CACHE
         const unsigned lx = (unsigned)(ijk[0] - lo[0]), ly = (unsigned)(ijk[1] - lo[1]),
                        lz = (unsigned)(ijk[2] - lo[2]);
         if ((lx | ly | lz) >= 8u) { // not the cached leaf (Accessor fast path, sparse.hpp:229-233)
@@ -212,7 +225,7 @@ struct VdbCursor {
                 return q;
             }
             const int ci = ((((ijk[2] >> 3) & 15) * 16 + ((ijk[1] >> 3) & 15)) * 16) + ((ijk[0] >> 3) & 15);
-            const int32_t code = __ldg(g.table + (int64_t)node * 4096 + ci); // child table
+            const int32_t code = table_at(g, node, ci); // child table
             if (code < 0) { // tile child (:205-208)
                 q.occ = code == kTileOccupied;
                 q.level = LV_LEAF_TILE;
@@ -230,6 +243,27 @@ struct VdbCursor {
         q.level = LV_VOXEL;
         q.ext = 1;
         return q;
+#else
+        // Uniform walk, no per-lane cache: root -> child table -> leaf word for every lane and
+        // every query, the loads made unconditional by clamping to valid entries and the answer
+        // picked with selects.  A per-lane leaf cache makes the miss path divergent: neighbouring
+        // rays leave their leaves on different iterations, so most warp iterations ran the
+        // ~45-instruction miss path for a handful of lanes (ncu: 3-10 of 32 active).
+        const bool inb = in_bounds(g, ijk);
+        const int region = inb ? ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7) : 0;
+        const int32_t node = __ldg(g.root + region);
+        const int ci = ((((ijk[2] >> 3) & 15) * 16 + ((ijk[1] >> 3) & 15)) * 16) + ((ijk[0] >> 3) & 15);
+        const int32_t code = table_at(g, node < 0 ? 0 : node, ci);
+        const uint64_t w = __ldg(g.leaves + (int64_t)(code < 0 ? 0 : code) * 8 + (ijk[2] & 7));
+        const bool bit = (w >> (((ijk[1] & 7) << 3) | (ijk[0] & 7))) & 1ull;
+        const bool leafv = inb && node >= 0 && code >= 0;
+        const bool tile = inb && node >= 0 && code < 0;
+        q.ext = leafv ? 1 : (tile ? 8 : 128);
+        q.level = !inb ? LV_ROOT_TILE : (node < 0 ? LV_INTERNAL_TILE : (code < 0 ? LV_LEAF_TILE : LV_VOXEL));
+        // root tile: empty; collapsed region: its value; tile child: its value; leaf: the bit
+        q.occ = inb && (node < 0 ? node == kRootOccupied : (code < 0 ? code == kTileOccupied : bit));
+        return q;
+#endif
     }
 };
 
@@ -376,12 +410,6 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
 #ifndef SOGK_HDDA_SMEM
 #define SOGK_HDDA_SMEM 1
 #endif
-#ifndef SOGK_VOXEL_FAST
-#define SOGK_VOXEL_FAST 1 // incremental exact stepping through voxel-level nodes (NodeAn::next)
-#endif
-#ifndef SOGK_VF_CACHE
-#define SOGK_VF_CACHE 1 // keep the voxel exit-plane times across iterations (else recompute)
-#endif
 // Kernels using the node analyzers or the cascade launch 1-D blocks of at most kGeomBlock
 // threads (per-thread shared-memory columns).
 constexpr int kGeomBlock = 128;
@@ -391,9 +419,6 @@ constexpr int kGeomBlock = 128;
 struct HddaGeomSmem {
     double e[3][kGeomBlock], dv[3][kGeomBlock], iv[3][kGeomBlock];
     double te[kGeomBlock], tx[kGeomBlock];
-    double mg[3][kGeomBlock]; // voxel fast path: re-derivation safety margin per axis (time)
-    double tp[3][kGeomBlock]; // voxel fast path: crossing time of the axis's last stepped plane
-    double tv[3][kGeomBlock]; // voxel fast path: exit-plane times of the current voxel
     int m[3][kGeomBlock];
 };
 __device__ __forceinline__ HddaGeomSmem& hdda_geom() {
@@ -414,9 +439,6 @@ struct NodeAn {
     __device__ __forceinline__ double& DV(int a) { return hdda_geom().dv[a][threadIdx.x]; }
     __device__ __forceinline__ double& IV(int a) { return hdda_geom().iv[a][threadIdx.x]; }
     __device__ __forceinline__ int& M(int a) { return hdda_geom().m[a][threadIdx.x]; }
-    __device__ __forceinline__ double& MG(int a) { return hdda_geom().mg[a][threadIdx.x]; }
-    __device__ __forceinline__ double& TP(int a) { return hdda_geom().tp[a][threadIdx.x]; }
-    __device__ __forceinline__ double& TV(int a) { return hdda_geom().tv[a][threadIdx.x]; }
     __device__ __forceinline__ double& TE() { return hdda_geom().te[threadIdx.x]; }
     __device__ __forceinline__ double& TX() { return hdda_geom().tx[threadIdx.x]; }
     __device__ __forceinline__ double TE() const { return hdda_geom().te[threadIdx.x]; }
@@ -425,10 +447,6 @@ struct NodeAn {
     double e[3], dv[3], iv[3]; // mirrored entry, |dir|, 1/|dir|
     int m[3];                  // -1 on mirrored axes, else 0
     double t_enter, t_exit;
-    double mg[3], tp[3], tv[3];
-    __device__ __forceinline__ double& MG(int a) { return mg[a]; }
-    __device__ __forceinline__ double& TP(int a) { return tp[a]; }
-    __device__ __forceinline__ double& TV(int a) { return tv[a]; }
     __device__ __forceinline__ double& E(int a) { return e[a]; }
     __device__ __forceinline__ double& DV(int a) { return dv[a]; }
     __device__ __forceinline__ double& IV(int a) { return iv[a]; }
@@ -447,17 +465,12 @@ struct NodeAn {
     bool done;
     bool undefined;
     VdbCursor cur;
-    // voxel fast path (SOGK_VOXEL_FAST): per-axis state for the re-derivation proof (the
-    // current voxel's exit-plane times live in the TV columns)
-    unsigned fstate; // bit 0: TV valid; bit 1: state known (fast path allowed); bits 2..4:
-                     // axis a's lower bound still to be proven (its cell came from a step)
 
     __device__ __forceinline__ void init(const Ray& r, const GridDev& g, int cap) {
         lookups = steps = 0;
         undefined = false;
         spin_cap = cap;
         degenerate = 0;
-        fstate = 0;
         cur.reset();
         Geom geom;
         geom.init(r, g);
@@ -487,35 +500,10 @@ struct NodeAn {
                 M(a) = 0;
             }
         }
-#if SOGK_VOXEL_FAST
-        // Re-derivation margin (time units), see next(): with u = 2^-53, |grid_coord error| <=
-        // 5.1 u R and |plane_t - exact crossing| <= 1.01 u |t| + 6.1 u R / |dir|, R bounding the
-        // mirrored coordinates; 2^-50 T and 2^-46 R / |dir| cover both with room to spare.
-        const double T = 2.0 * ((geom.t_exit > geom.t_enter) ? geom.t_exit : geom.t_enter) + 1.0;
-        int rmax = g.res[0] > g.res[1] ? g.res[0] : g.res[1];
-        rmax = rmax > g.res[2] ? rmax : g.res[2];
-        const double R = (double)rmax + 2.0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-            MG(a) = geom.step[a] != 0 ? T * 0x1p-50 + R * 0x1p-46 * fabs(geom.inv[a]) : 0.0;
-#endif
     }
 
     // One iteration of HddaTraversal::next's loop (:213-248): 1 = event, 0 = end,
     // -1 = degenerate iteration consumed (call again).
-    //
-    // Voxel fast path (SOGK_VOXEL_FAST).  Inside mixed leaves every node is a voxel (extent 1),
-    // whose exit plane on each axis depends on that axis's cell only, and a step changes one
-    // axis: the other axes keep their exit-plane times (same inputs, same bits) and their cells
-    // -- unless the reference's re-derivation at t1 (cell_after_crossing, :91-104) lands
-    // elsewhere, which it can only do near a tie.  The re-derived cell of a non-stepped axis
-    // equals the current one when grid_coord(t1) is provably inside [lo, lo + 1): upper side
-    // t1 + MG < (its exit-plane time), lower side t1 > TP + MG for an axis whose cell came from a
-    // step at TP (a cell that came from a re-derivation, or passed this test once, keeps its
-    // lower side: grid_coord is monotone in t, each FP op being monotone).  Then the iteration
-    // is one plane_t for the stepped axis and no re-derivation; anything else -- ties, near-
-    // ties, degenerate crossings, non-voxel nodes, the final event -- takes the exact path.
-    // Events, cells and counters are the reference's bit for bit.
     __device__ __forceinline__ int next(const GridDev& g, Event& ev) {
         if (done) return 0;
         Query q;
@@ -537,26 +525,11 @@ struct NodeAn {
         const double te = TE();
         double tc[3];
         int pl[3];
-#if SOGK_VOXEL_FAST
-        // Both fast-path decisions are warp votes: a SIMT warp pays for every path one of its
-        // lanes takes, so the shortcut is taken only when every active lane can take it
-        // (coherent rays through mixed leaves), never as a divergent side path.
-        const bool vox = q.ext == 1;
-        const bool cached = __all_sync(__activemask(), SOGK_VF_CACHE && vox && (fstate & 1u));
-#else
-        constexpr bool cached = false;
-#endif
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const int lo = CD ? ijk[a] - half : (ijk[a] & -q.ext);
             ev.ijk[a] = lo;
             pl[a] = (lo ^ M(a)) + (M(a) ? 1 : q.ext);
-#if SOGK_VOXEL_FAST
-            if (cached) {
-                tc[a] = TV(a);
-                continue;
-            }
-#endif
             tc[a] = te + ((double)pl[a] - E(a)) * IV(a);
         }
         double t1;
@@ -572,41 +545,6 @@ struct NodeAn {
             return 1;
         }
         const bool degen = t1 <= t_cur; // degenerate corner crossing (:238-241)
-#if SOGK_VOXEL_FAST
-        {
-            bool ok = vox && !degen && (fstate & 2u);
-            unsigned lower = fstate;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                if (a == axis || DV(a) == 0.0) continue; // stepped or static axis
-                const double mg = MG(a);
-                ok = ok && (t1 + mg < tc[a]);
-                if (lower & (4u << a)) {
-                    ok = ok && (t1 > TP(a) + mg);
-                    lower &= ~(4u << a);
-                }
-            }
-            if (__all_sync(__activemask(), ok)) {
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    if (a != axis) {
-                        TV(a) = tc[a];
-                        continue;
-                    }
-                    ijk[a] = pl[a] ^ M(a);
-                    TV(a) = te + ((double)(pl[a] + 1) - E(a)) * IV(a); // the next voxel's plane
-                    TP(a) = t1;
-                }
-                fstate = (lower | 3u) | (4u << axis);
-                degenerate = 0;
-                ev.t0 = t_cur;
-                ev.t1 = t1;
-                ++steps;
-                t_cur = t1;
-                return 1;
-            }
-        }
-#endif
         // cell_after_crossing (:91-104) at t_cur (degenerate) or t1, all axes
         // evaluated and the stepped one overridden
         const double dt = (degen ? t_cur : t1) - te;
@@ -615,12 +553,6 @@ struct NodeAn {
             const int c = __double2int_rd(E(a) + dt * DV(a)) ^ M(a);
             ijk[a] = (a == axis) ? (pl[a] ^ M(a)) : c;
         }
-#if SOGK_VOXEL_FAST
-        // every cell is now a re-derivation at t1 (or t_cur) except the stepped axis's, set at
-        // its crossing time t1
-        TP(axis) = t1;
-        fstate = 2u | (4u << axis);
-#endif
         if (degen) {
             // the reference spins forever at exact edge crossings
             if (++degenerate > spin_cap) {
@@ -648,7 +580,6 @@ struct NodeAn {
     __device__ __forceinline__ void restore(const GridDev&, const int in_ijk[3], double in_t) {
         done = false;
         degenerate = 0;
-        fstate = 0; // the first iteration after a resume is exact
         t_cur = in_t;
         ijk[0] = in_ijk[0];
         ijk[1] = in_ijk[1];

@@ -47,6 +47,8 @@ struct GridDev {
     const uint64_t* leaves;
     const int32_t* table;
     const int32_t* dist;   // DistanceGrid (distance.hpp:15-43): chessboard distance per voxel
+    int smem_tab;          // launch-local: the child table of this single-region VDB is staged
+                           // in the kernel's dynamic shared memory (sogk_dyn_smem)
 };
 
 struct SamplerDev {

@@ -33,6 +33,9 @@ constexpr int kWriteBlock = 128;
 #ifndef SOGK_COUNT_MINB
 #define SOGK_COUNT_MINB 1 // pass-1 min resident blocks per SM (register cap), A/B-tunable
 #endif
+#ifndef SOGK_SMEM_TABLE
+#define SOGK_SMEM_TABLE 1 // pass 1 stages a single-region VDB's child table in shared memory
+#endif
 
 // ---------------------------------------------------------------------------
 // warp / block scans
@@ -176,6 +179,13 @@ __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MIN
     count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
                  int32_t* __restrict__ counters, const SlabDev S) {
+    if (s.lv[0].smem_tab) { // stage the single-region child table (16 KB) in shared memory
+        const int32_t node0 = __ldg(s.lv[0].root);
+        const int4* tsrc = reinterpret_cast<const int4*>(s.lv[0].table + (int64_t)(node0 < 0 ? 0 : node0) * 4096);
+        int4* tdst = reinterpret_cast<int4*>(sogk_dyn_smem);
+        for (int i = threadIdx.x; i < 1024; i += kBlock) tdst[i] = __ldg(tsrc + i);
+        __syncthreads();
+    }
     const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     Stats5 acc;
     if (j < n) {
@@ -770,8 +780,16 @@ struct Launch {
                              int64_t* stats, uint8_t* status, int32_t* counters, const SlabDev& S,
                              cudaStream_t st) {
         const int64_t blocks = (n + kBlock - 1) / kBlock;
+        // upper VDB level in shared memory: the child table of a single-region grid (128^3 and
+        // below) is staged per block; larger grids read it through L1 / L2
+        SamplerDev s2 = s;
+        size_t dyn = 0;
+        if (SOGK_SMEM_TABLE && AN == SOGK_HDDA && !CASC && s.lv[0].R[0] * s.lv[0].R[1] * s.lv[0].R[2] == 1) {
+            s2.lv[0].smem_tab = 1;
+            dyn = 4096 * sizeof(int32_t);
+        }
         count_kernel<AN, CASC, BR, SCH, Src>
-            <<<(unsigned)blocks, kBlock, 0, st>>>(s, src, n, packed, stats, status, counters, S);
+            <<<(unsigned)blocks, kBlock, dyn, st>>>(s2, src, n, packed, stats, status, counters, S);
         return cudaGetLastError();
     }
     template <int AN, bool CASC, bool BR, int SCH>

@@ -1,10 +1,9 @@
-"""Stress for the node analyzers' voxel fast path (sogk_device.cuh NodeAn::next,
-SOGK_VOXEL_FAST): through mixed leaves the HDDA / CD step keeps the other axes' exit planes and
-cells unless the reference's re-derivation could land elsewhere (ties, near-ties, degenerate
-crossings), where it takes the exact path.  These inputs are built to hit exactly those cases
--- rays through voxel corners, edges and faces with axis-aligned and diagonal directions, on
-fully mixed grids -- plus iid random grids at every occupancy of the cfg5 sweep; every output
-(events, samples, cells, counters, spin flags) is compared bit for bit with the C oracle."""
+"""Tie / near-tie stress of the node analyzers (HDDA, CD) and the branch kernel's probe: rays
+through voxel corners, edges and faces with axis-aligned and diagonal directions on fully mixed
+grids (every crossing an exact or near tie, the reference's degenerate re-derivation and its
+edge-crossing spin), plus iid random grids at the occupancies of the cfg5 sweep; every output
+(events, samples, cells, counters, spin flags) is compared bit for bit with the C oracle.
+(This suite found the branch kernel's probe on out-of-grid root-tile events, step_event.)"""
 import itertools
 import math
 
