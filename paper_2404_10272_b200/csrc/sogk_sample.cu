@@ -468,7 +468,7 @@ constexpr int kStageW = SOGK_STAGE_W;
 #ifndef SOGK_GATHER_MINB
 #define SOGK_GATHER_MINB 1
 #endif
-template <int SCH>
+template <int SCH, bool VEC>
 __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
     gather_kernel(const __grid_constant__ SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
                   const SlabDev S, int64_t ray_index_base, const Out o) {
@@ -633,7 +633,10 @@ __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
             }
             __syncthreads();
             const int m = (int)(we - w);
-            for (int p = tid; p < m; p += kGather) { // coalesced: consecutive lanes, consecutive samples
+            // coalesced stores; with aligned outputs the body goes out as 128-bit stores of four
+            // consecutive samples per thread (the scalar head / tail align it to 4 samples)
+            const int h = VEC ? (int)((-w) & 3) < m ? (int)((-w) & 3) : m : m;
+            for (int p = tid; p < h; p += kGather) {
                 const long long g = w + p;
                 const double t = s_t[p];
                 __stcs(o.t_starts + g, t);
@@ -641,6 +644,43 @@ __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
                 if (o.ray_indices) __stcs(o.ray_indices + g, s_ri[p]);
                 if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, s_ce[p]);
                 if (o.levels) o.levels[g] = s_lv[p];
+            }
+            if (VEC) {
+                const int nq = (m - h) >> 2;
+                for (int qd = tid; qd < nq; qd += kGather) {
+                    const int p = h + 4 * qd;
+                    const long long g = w + p; // multiple of 4
+                    const double a0 = s_t[p], a1 = s_t[p + 1], a2 = s_t[p + 2], a3 = s_t[p + 3];
+                    double2* ts = reinterpret_cast<double2*>(o.t_starts + g);
+                    __stcs(ts, make_double2(a0, a1));
+                    __stcs(ts + 1, make_double2(a2, a3));
+                    if (o.t_ends) {
+                        double2* te = reinterpret_cast<double2*>(o.t_ends + g);
+                        __stcs(te, make_double2(a0 + ladder_step<SCH>(a0, s.dt0, s.growth),
+                                                a1 + ladder_step<SCH>(a1, s.dt0, s.growth)));
+                        __stcs(te + 1, make_double2(a2 + ladder_step<SCH>(a2, s.dt0, s.growth),
+                                                    a3 + ladder_step<SCH>(a3, s.dt0, s.growth)));
+                    }
+                    if (o.ray_indices)
+                        __stcs(reinterpret_cast<int4*>(o.ray_indices + g),
+                               make_int4(s_ri[p], s_ri[p + 1], s_ri[p + 2], s_ri[p + 3]));
+                    if (o.cells)
+                        __stcs(reinterpret_cast<uint4*>(o.cells + g),
+                               make_uint4(s_ce[p], s_ce[p + 1], s_ce[p + 2], s_ce[p + 3]));
+                    if (o.levels)
+                        *reinterpret_cast<uint32_t*>(o.levels + g) =
+                            (uint32_t)s_lv[p] | ((uint32_t)s_lv[p + 1] << 8) | ((uint32_t)s_lv[p + 2] << 16) |
+                            ((uint32_t)s_lv[p + 3] << 24);
+                }
+                for (int p = h + 4 * nq + tid; p < m; p += kGather) {
+                    const long long g = w + p;
+                    const double t = s_t[p];
+                    __stcs(o.t_starts + g, t);
+                    if (o.t_ends) __stcs(o.t_ends + g, t + ladder_step<SCH>(t, s.dt0, s.growth));
+                    if (o.ray_indices) __stcs(o.ray_indices + g, s_ri[p]);
+                    if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, s_ce[p]);
+                    if (o.levels) o.levels[g] = s_lv[p];
+                }
             }
             __syncthreads();
         }
@@ -805,7 +845,10 @@ struct Launch {
             return cudaGetLastError();
         }
         const unsigned gb = (unsigned)((n + kGather - 1) / kGather);
-        gather_kernel<SCH><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
+        if (vec)
+            gather_kernel<SCH, true><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
+        else
+            gather_kernel<SCH, false><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
         const unsigned tg = tail_grid(n);
         if (vec)
             tail_kernel<AN, CASC, BR, SCH, true, Src><<<tg, kWriteBlock, 0, st>>>(s, src, packed, *S, base, o);
