@@ -309,6 +309,14 @@ class Workload:
         return P.Camera(spec["pos"], (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, self.width, self.height)
 
 
+def host_expand_link_bytes() -> int:
+    """PCIe bytes per sample of the north-star outputs through sogk_sample_host: t_starts always;
+    t_ends (8) and ray_indices (4) unless expanded on host threads (SOGK_HOST_EXPAND, sogk_api.cpp)."""
+    e = os.environ.get("SOGK_HOST_EXPAND", "all")
+    mode = 0 if e.startswith("0") else 1 if e.startswith("r") else 2 if e.startswith("t") else 3
+    return 8 + (0 if mode & 2 else 8) + (0 if mode & 1 else 4)
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -673,8 +681,7 @@ def run_gpu(args):
         e2e = dict(full_seconds=e2e_full_s, lean_seconds=e2e_lean_s, h2d=nr * 64 * n_obj, workers=n_workers,
                    # t_ends / ray_indices are expanded on host threads from the downloaded
                    # t_starts + packed_info (sogk_sample_host, SOGK_HOST_EXPAND): not on the link
-                   full_d2h=samples0 * (8 if os.environ.get("SOGK_HOST_EXPAND", "1") != "0" else 20) / args.steps
-                   + nr * 16 * n_obj,
+                   full_d2h=samples0 * host_expand_link_bytes() / args.steps + nr * 16 * n_obj,
                    lean_d2h=samples0 * 8 / args.steps + nr * (16 + 12) * n_obj)
 
     # --- max over ranks

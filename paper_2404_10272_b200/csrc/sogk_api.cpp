@@ -1665,10 +1665,15 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     // t_starts / packed_info of each finished chunk, while the next chunks are on the GPU and
     // the PCIe link -- the device->host link is the bound of this call, and this cuts its bytes
     // per sample from 20 to 8.  Same IEEE operation (one add, no FMA), so the bytes are
-    // identical to the device's.  SOGK_HOST_EXPAND=0: download them instead.
-    static const bool kExpand = [] {
+    // identical to the device's.  SOGK_HOST_EXPAND: "all" (both), "ri" (ray_indices only,
+    // t_ends downloaded), "0" (download both); default "all".
+    static const int kExpand = [] { // bit 0: ray_indices on the host, bit 1: t_ends on the host
         const char* e = std::getenv("SOGK_HOST_EXPAND");
-        return !(e && e[0] == '0');
+        if (!e) return 3;
+        if (e[0] == '0') return 0;
+        if (e[0] == 'r') return 1;
+        if (e[0] == 't') return 2;
+        return 3;
     }();
     static const int kExpandThreads = [] {
         const char* e = std::getenv("SOGK_HOST_THREADS");
@@ -1676,7 +1681,9 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         const int hw = int(std::thread::hardware_concurrency());
         return int(v >= 1 && v <= 64 ? v : std::max(1, std::min(8, hw / 2)));
     }();
-    const bool expand = kExpand && h_t_starts && (h_t_ends || h_ray_indices);
+    const bool exp_ri = (kExpand & 1) && h_t_starts && h_ray_indices;
+    const bool exp_te = (kExpand & 2) && h_t_starts && h_t_ends;
+    const bool expand = exp_ri || exp_te;
     // n / 8 rays per chunk, at most 512 K: big calls get a deeper pipeline (shorter fill and
     // drain; 2^24 probe rays: 32 chunks, +4.5 % e2e over 8)
     const int64_t chunk = std::max<int64_t>(65536, std::min<int64_t>((n + kChunks - 1) / kChunks, 1 << 19));
@@ -1685,8 +1692,8 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     const size_t b_rays = al(size_t(n) * 64), b_packed = al(size_t(n) * 16),
                  b_stats = al(size_t(std::max<int64_t>(nchunks, 1)) * SOGK_STATS_LEN * 8),
                  b_status = al(size_t(n)), b_ctr = al(size_t(n) * 12);
-    const size_t b_ts = al(size_t(capacity) * 8), b_te = expand ? 0 : al(size_t(capacity) * 8),
-                 b_ri = expand ? 0 : al(size_t(capacity) * 4), b_ce = al(size_t(capacity) * 4),
+    const size_t b_ts = al(size_t(capacity) * 8), b_te = exp_te ? 0 : al(size_t(capacity) * 8),
+                 b_ri = exp_ri ? 0 : al(size_t(capacity) * 4), b_ce = al(size_t(capacity) * 4),
                  b_lv = al(size_t(capacity));
     const size_t need = b_rays + b_packed + b_stats + b_status + b_ctr + b_ts + b_te + b_ri + b_ce + b_lv;
     if (need > s->hb_bytes) {
@@ -1753,14 +1760,13 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
             if (a >= b) return;
             const int64_t lo = h_packed_info[2 * (r0 + a)];
             const int64_t hi = h_packed_info[2 * (r0 + b - 1)] + h_packed_info[2 * (r0 + b - 1) + 1];
-            if (h_ray_indices) {
+            if (exp_ri) {
                 for (int64_t r = r0 + a; r < r0 + b; ++r) {
                     const int64_t off = h_packed_info[2 * r], cnt = h_packed_info[2 * r + 1];
-                    const int32_t ri = int32_t(ray_index_base + r);
-                    for (int64_t k = 0; k < cnt; ++k) h_ray_indices[off + k] = ri;
+                    std::fill_n(h_ray_indices + off, cnt, int32_t(ray_index_base + r));
                 }
             }
-            if (h_t_ends) {
+            if (exp_te) {
                 const double* ts = h_t_starts;
                 double* te = h_t_ends;
                 if (linear) {
@@ -1822,14 +1828,14 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
             if (tot > 0) {
                 const int st = write_impl(s, d_rays + 8 * r0, nullptr, 0, m, d_packed + 2 * r0,
                                           tokens[size_t(c)], ray_index_base + r0, d_ts,
-                                          (h_t_ends && !expand) ? d_te : nullptr,
-                                          (h_ray_indices && !expand) ? d_ri : nullptr, h_cells ? d_ce : nullptr,
+                                          (h_t_ends && !exp_te) ? d_te : nullptr,
+                                          (h_ray_indices && !exp_ri) ? d_ri : nullptr, h_cells ? d_ce : nullptr,
                                           h_levels ? d_lv : nullptr, L);
                 if (st) return st;
                 const size_t o = size_t(base), tb = size_t(tot);
                 if (h_t_starts) CK(cudaMemcpyAsync(h_t_starts + o, d_ts + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
-                if (h_t_ends && !expand) CK(cudaMemcpyAsync(h_t_ends + o, d_te + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
-                if (h_ray_indices && !expand) CK(cudaMemcpyAsync(h_ray_indices + o, d_ri + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_t_ends && !exp_te) CK(cudaMemcpyAsync(h_t_ends + o, d_te + o, tb * 8, cudaMemcpyDeviceToHost, L), "D2H");
+                if (h_ray_indices && !exp_ri) CK(cudaMemcpyAsync(h_ray_indices + o, d_ri + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
                 if (h_cells) CK(cudaMemcpyAsync(h_cells + o, d_ce + o, tb * 4, cudaMemcpyDeviceToHost, L), "D2H");
                 if (h_levels) CK(cudaMemcpyAsync(h_levels + o, d_lv + o, tb, cudaMemcpyDeviceToHost, L), "D2H");
             }

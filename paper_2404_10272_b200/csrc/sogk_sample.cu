@@ -34,7 +34,7 @@ constexpr int kWriteBlock = 128;
 #define SOGK_COUNT_MINB 1 // pass-1 min resident blocks per SM (register cap), A/B-tunable
 #endif
 #ifndef SOGK_SMEM_TABLE
-#define SOGK_SMEM_TABLE 1 // pass 1 stages a single-region VDB's child table in shared memory
+#define SOGK_SMEM_TABLE 0 // 1: pass 1 stages a single-region VDB's child table in shared memory
 #endif
 
 // ---------------------------------------------------------------------------
@@ -464,9 +464,12 @@ constexpr int kGather = 256;
 #define SOGK_STAGE_W 2048 // samples per staging window (17 B each in shared memory)
 #endif
 constexpr int kStageW = SOGK_STAGE_W;
+#ifndef SOGK_GATHER_VEC
+#define SOGK_GATHER_VEC 1 // 128-bit stores of four samples per thread when the outputs are aligned
+#endif
 
 #ifndef SOGK_GATHER_MINB
-#define SOGK_GATHER_MINB 1
+#define SOGK_GATHER_MINB 4 // <= 64 registers: 4 blocks of 256 per SM
 #endif
 template <int SCH, bool VEC>
 __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
@@ -845,7 +848,7 @@ struct Launch {
             return cudaGetLastError();
         }
         const unsigned gb = (unsigned)((n + kGather - 1) / kGather);
-        if (vec)
+        if (vec && SOGK_GATHER_VEC)
             gather_kernel<SCH, true><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
         else
             gather_kernel<SCH, false><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
