@@ -465,7 +465,7 @@ constexpr int kGather = 256;
 #endif
 constexpr int kStageW = SOGK_STAGE_W;
 #ifndef SOGK_GATHER_VEC
-#define SOGK_GATHER_VEC 1 // 128-bit stores of four samples per thread when the outputs are aligned
+#define SOGK_GATHER_VEC 0 // 1: 128-bit stores of four samples per thread (A/B: pass 2 +11 % time, off)
 #endif
 
 #ifndef SOGK_GATHER_MINB
