@@ -312,7 +312,7 @@ class Workload:
 def host_expand_link_bytes() -> int:
     """PCIe bytes per sample of the north-star outputs through sogk_sample_host: t_starts always;
     t_ends (8) and ray_indices (4) unless expanded on host threads (SOGK_HOST_EXPAND, sogk_api.cpp)."""
-    e = os.environ.get("SOGK_HOST_EXPAND", "all")
+    e = os.environ.get("SOGK_HOST_EXPAND", "t")
     mode = 0 if e.startswith("0") else 1 if e.startswith("r") else 2 if e.startswith("t") else 3
     return 8 + (0 if mode & 2 else 8) + (0 if mode & 1 else 4)
 
@@ -794,9 +794,10 @@ def run_gpu(args):
         line["e2e"] = {"value": total_rays / e2e["full_seconds"], "unit": "rays/s",
                        "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["full_d2h"]),
                        "api": "sogk_sample_host: pinned host rays in; out the north-star packed intervals "
-                              "(packed_info, t_starts, t_ends, ray_indices) in host memory; t_starts and "
-                              "packed_info cross PCIe, t_ends = t + step(t) and ray_indices are expanded "
-                              "from them on host threads while later chunks are in flight",
+                              "(packed_info, t_starts, t_ends, ray_indices) in host memory; "
+                              f"{host_expand_link_bytes()} PCIe bytes per sample (SOGK_HOST_EXPAND: t_ends = "
+                              "t + step(t) and/or ray_indices expanded on host threads from the downloaded "
+                              "t_starts / packed_info while later chunks are in flight)",
                        "host_threads": e2e["workers"],
                        "lean": {"value": total_rays / e2e["lean_seconds"], "unit": "rays/s",
                                 "d2h_bytes_per_step": int(e2e["lean_d2h"]),

@@ -202,10 +202,11 @@ int sogk_sample_count(sogk_sampler* s, const double* d_rays, int64_t n, int64_t*
                       int64_t* d_stats, uint8_t* d_status, int32_t* d_counters, void* stream);
 /* Pass 2: writes the packed samples at the offsets of d_packed_info.  Buffers must hold
  * stats[SOGK_STAT_TOTAL_SAMPLES] entries; d_cells / d_levels / d_t_ends / d_ray_indices
- * may be NULL.  Pass 1 leaves each ray's first samples in the sampler's workspace (one
- * fixed slab per ray, SOGK_SLAB entries, default 256); a write that directly follows the
- * count of the same rays on the same sampler only moves them into place, and rays whose
- * samples did not fit resume their traversal.  Any other write traverses from scratch.
+ * may be NULL.  Pass 1 leaves each ray's sample runs in the workspace of the stream (a
+ * fixed slab of run records per ray, SOGK_SLAB, default 128, reduced when 40 % of the free
+ * device memory cannot hold it); a write that directly follows the count of the same rays on
+ * the same sampler and stream only expands them into place, and rays whose runs did not fit
+ * resume their traversal.  Any other write traverses from scratch.
  * Calls on one sampler must therefore be ordered (one stream, or synchronised). */
 int sogk_sample_write(sogk_sampler* s, const double* d_rays, int64_t n,
                       const int64_t* d_packed_info, int64_t ray_index_base, double* d_t_starts,

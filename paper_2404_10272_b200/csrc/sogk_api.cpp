@@ -223,21 +223,22 @@ struct Workspace {
     const void* rays = nullptr;
     int64_t first = -1, n = -1;
     bool cam = false;
+    int64_t C = 0; // run records per ray the slabs are laid out with (set by the claiming count)
 };
 static std::atomic<uint64_t> g_sampler_ids{0};
 static std::atomic<uint64_t> g_count_tokens{0};
-// Pass-1 slab budget per workspace: SOGK_SLAB_BUDGET_GB, else the larger of 8 GiB and 35 % of
-// the device memory free when first asked (a smaller slab only sends more rays to tail_kernel)
-static double slab_budget_bytes() {
-    static const double b = [] {
-        if (const char* e = std::getenv("SOGK_SLAB_BUDGET_GB")) return std::max(0.0, std::atof(e)) * double(1ull << 30);
-        size_t fr = 0, tot = 0;
-        double v = 8.0 * double(1ull << 30);
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) v = std::max(v, 0.35 * double(fr));
-        else cudaGetLastError();
-        return v;
-    }();
-    return b;
+// Pass-1 slab budget for a workspace that has to grow: SOGK_SLAB_BUDGET_GB, else 40 % of the
+// device memory free at that moment (counting the workspace's own current block, which is
+// released first) and at least 2 GiB.  Asked only when the full slab (C = SOGK_SLAB, 128) does
+// not fit the workspace already held; a smaller slab only sends more rays to tail_kernel.
+static double slab_budget_bytes(size_t held) {
+    if (const char* e = std::getenv("SOGK_SLAB_BUDGET_GB")) return std::max(0.0, std::atof(e)) * double(1ull << 30);
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return 8.0 * double(1ull << 30);
+    }
+    return std::max(2.0 * double(1ull << 30), 0.4 * (double(fr) + double(held)));
 }
 static std::mutex g_ws_mu;
 static std::map<std::pair<int, void*>, Workspace>& ws_registry() {
@@ -251,24 +252,6 @@ static Workspace* workspace_peek(void* stream) {
     auto it = ws_registry().find({dev, stream});
     return it == ws_registry().end() ? nullptr : &it->second;
 }
-static int workspace_for(void* stream, size_t need, Workspace** out) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_ws_mu);
-    Workspace& w = ws_registry()[{dev, stream}];
-    if (w.bytes < need) {
-        cudaFree(w.ptr); // synchronous: work still reading it has finished
-        w.ptr = nullptr;
-        w.bytes = 0;
-        w.owner = 0; // whatever it held is gone
-        w.token = 0;
-        CK(cudaMalloc(&w.ptr, need), "sampler workspace");
-        w.bytes = need;
-    }
-    *out = &w;
-    return SOGK_OK;
-}
-
 // Render scratch, one per (device, stream) like the workspaces (work on a stream is ordered;
 // the mutex covers host threads sharing a stream): [stats 256 B | packed n x 16 | rays n x 64]
 // and, per sample, t 8 B | ray index 4 B | shaded 32 B.
@@ -382,42 +365,59 @@ struct sogk_sampler {
     int ray_order = 0; // 1: pass 1 processes buffer rays binned by entry cell and direction
     int64_t slab_cap = 128; // C: run records per ray (SOGK_SLAB; 0 = resume-only)
 
-    int64_t cap_for(int64_t n) const {
+    int64_t cap_for(int64_t n, double budget) const {
         // keep the slabs within the budget; a smaller slab only sends more rays to
         // tail_kernel (exact either way)
-        const double budget = slab_budget_bytes();
         int64_t c = slab_cap;
         while (c > 0 && double(n) * double(c) * 16.0 > budget) c -= 4;
         return c < 0 ? 0 : c;
     }
     static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
     // workspace = [scan tile states | counters (64 B) | resume states | overflow list |
-    //              run counts | run slabs]
-    size_t need_bytes(int64_t n) const {
-        const size_t e = size_t(n) * size_t(cap_for(n));
+    //              run counts | run slabs (C per ray) | ray-binning scratch]
+    size_t need_bytes(int64_t n, int64_t C) const {
+        const size_t e = size_t(n) * size_t(C);
         return scan_off(n) + al(resume_bytes(n)) + 2 * al(size_t(n) * 4) + al(e * sizeof(RunRec)) +
                (ray_order ? bin_scratch_bytes(n) : 0);
     }
     // ray-binning scratch, after the slabs
     void* bin_scratch(const Workspace* w, int64_t n) const {
-        const size_t e = size_t(n) * size_t(cap_for(n));
+        const size_t e = size_t(n) * size_t(w->C);
         return static_cast<char*>(w->ptr) + scan_off(n) + al(resume_bytes(n)) + 2 * al(size_t(n) * 4) +
                al(e * sizeof(RunRec));
     }
     // the (device, stream) workspace, grown to fit n rays and tagged for this count
     int claim_ws(int64_t n, void* stream, const void* rays, const void* packed, bool cam,
                  int64_t first, Workspace** out) {
-        Workspace* w = nullptr;
-        int st = workspace_for(stream, need_bytes(n), &w);
-        if (st) return st;
-        w->token = ++g_count_tokens;
-        w->owner = id;
-        w->rays = rays;
-        w->packed = packed;
-        w->cam = cam;
-        w->first = first;
-        w->n = n;
-        *out = w;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        Workspace& w = ws_registry()[{dev, stream}];
+        int64_t C = slab_cap;
+        size_t need = need_bytes(n, C);
+        if (w.bytes < need) { // the full slab does not fit what is held: size it from free memory
+            C = cap_for(n, slab_budget_bytes(w.bytes));
+            int64_t fit = slab_cap; // or keep the largest slab the held block already fits
+            while (fit > C && need_bytes(n, fit) > w.bytes) fit -= 4;
+            C = std::max(C, fit);
+            need = need_bytes(n, C);
+        }
+        if (w.bytes < need) {
+            cudaFree(w.ptr); // synchronous: work still reading it has finished
+            w.ptr = nullptr;
+            w.bytes = 0;
+            CK(cudaMalloc(&w.ptr, need), "sampler workspace");
+            w.bytes = need;
+        }
+        w.C = C;
+        w.token = ++g_count_tokens;
+        w.owner = id;
+        w.rays = rays;
+        w.packed = packed;
+        w.cam = cam;
+        w.first = first;
+        w.n = n;
+        *out = &w;
         return SOGK_OK;
     }
     // the workspace holding this sampler's slabs for these rays, or nullptr; token != 0 must
@@ -440,7 +440,7 @@ struct sogk_sampler {
     SlabDev slab(const Workspace* w, int64_t n) const {
         char* p = static_cast<char*>(w->ptr) + scan_off(n);
         SlabDev S{};
-        S.C = cap_for(n);
+        S.C = w->C;
         S.resume = reinterpret_cast<Resume*>(p);
         p += al(resume_bytes(n));
         S.ovf_list = reinterpret_cast<uint32_t*>(p);
@@ -1666,10 +1666,11 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     // the PCIe link -- the device->host link is the bound of this call, and this cuts its bytes
     // per sample from 20 to 8.  Same IEEE operation (one add, no FMA), so the bytes are
     // identical to the device's.  SOGK_HOST_EXPAND: "all" (both), "ri" (ray_indices only,
-    // t_ends downloaded), "0" (download both); default "all".
+    // t_ends downloaded), "t" (t_ends only, ray_indices downloaded), "0" (download both);
+    // default "t" (the balance of PCIe and host memory traffic that measured best)
     static const int kExpand = [] { // bit 0: ray_indices on the host, bit 1: t_ends on the host
         const char* e = std::getenv("SOGK_HOST_EXPAND");
-        if (!e) return 3;
+        if (!e) return 2;
         if (e[0] == '0') return 0;
         if (e[0] == 'r') return 1;
         if (e[0] == 't') return 2;
@@ -1679,7 +1680,7 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         const char* e = std::getenv("SOGK_HOST_THREADS");
         const long v = e ? std::atol(e) : 0;
         const int hw = int(std::thread::hardware_concurrency());
-        return int(v >= 1 && v <= 64 ? v : std::max(1, std::min(8, hw / 4)));
+        return int(v >= 1 && v <= 64 ? v : std::max(1, std::min(8, hw / 2)));
     }();
     const bool exp_ri = (kExpand & 1) && h_t_starts && h_ray_indices;
     const bool exp_te = (kExpand & 2) && h_t_starts && h_t_ends;

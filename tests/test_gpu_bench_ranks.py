@@ -54,3 +54,23 @@ def test_two_ranks_concatenate_to_one(tmp_path, cfg):
         assert np.array_equal(cat.view(np.uint8), a[key].view(np.uint8)), key
     cnt = np.concatenate([p["packed_info"][:, 1] for p in parts])
     assert np.array_equal(cnt, a["packed_info"][:, 1])
+
+
+def test_two_ranks_default_config_full_line(tmp_path):
+    """The driver's scaling run: bench.py's default config (cfg2, views per rank, weak scaling)
+    with every leg (e2e through sogk_sample_host, render) under two ranks; rank 0 prints one
+    JSON line with the whole job's rays (two ranks' views)."""
+    import json
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--backend", "gloo", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["config"]["rays_per_step"] == 2 * 8 * 800 * 800
+    assert d["e2e"]["value"] > 0 and d["render"] is not None
+    assert d["value"] > 0 and d["gpu_launches"] > 0
