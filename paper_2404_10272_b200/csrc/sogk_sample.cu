@@ -464,12 +464,6 @@ constexpr int kGather = 256;
 #define SOGK_STAGE_W 2048 // samples per staging window (17 B each in shared memory)
 #endif
 constexpr int kStageW = SOGK_STAGE_W;
-#ifndef SOGK_GATHER_WARP
-#define SOGK_GATHER_WARP 1 // warp-independent pass 2 (gather_warp_kernel); 0: block-staged gather_kernel
-#endif
-#ifndef SOGK_WARP_W
-#define SOGK_WARP_W 256 // samples per warp staging window (17 B each in shared memory)
-#endif
 #ifndef SOGK_GATHER_VEC
 #define SOGK_GATHER_VEC 0 // 1: 128-bit stores of four samples per thread (A/B: pass 2 +11 % time, off)
 #endif
@@ -755,152 +749,6 @@ __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
     }
 }
 
-// pass 2, warp-independent form: every warp owns 32 consecutive rays (one contiguous output
-// range) and expands their runs with warp-level scans and shuffles only -- no block barrier,
-// which was the staged kernel's top stall (ncu: barrier) -- staging each output window of
-// kWarpW samples in its own shared-memory slice and storing it coalesced.
-constexpr int kWarpW = SOGK_WARP_W;
-
-template <int SCH>
-__global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
-    gather_warp_kernel(const __grid_constant__ SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
-                       const SlabDev S, int64_t ray_index_base, const Out o) {
-    __shared__ double s_t[kGather / 32][kWarpW];
-    __shared__ int32_t s_ri[kGather / 32][kWarpW];
-    __shared__ uint32_t s_ce[kGather / 32][kWarpW];
-    __shared__ uint8_t s_lv[kGather / 32][kWarpW];
-    constexpr int kShort = SOGK_GATHER_SHORT;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * kGather + (int64_t)wid * 32; // this warp's first ray
-    const int64_t r = r0 + lane;
-    long long off = 0;
-    int nr = 0, fill = 0;
-    if (r < n) {
-        const longlong2 pi = __ldg(reinterpret_cast<const longlong2*>(packed) + r);
-        const int raw = pi.y > 0 ? __ldg(S.nruns + r) : 0;
-        nr = raw & 0x7fffffff;
-        off = pi.x;
-        // every sample of the ray is in its runs, unless they overflowed the slab: then the
-        // slab covers the samples before the resume point (Resume::tag bits 8..31)
-        fill = raw < 0 ? (int)((uint32_t)S.resume[r].tag >> 8) : (int)pi.y;
-    }
-    const int incl = warp_incl_scan_i(nr);
-    const int roff = incl - nr;                                   // this ray's first run
-    const int total = __shfl_sync(0xffffffffu, incl, 31);         // the warp's runs
-    double* const wt = s_t[wid];
-    int32_t* const wri = s_ri[wid];
-    uint32_t* const wce = s_ce[wid];
-    uint8_t* const wlv = s_lv[wid];
-    for (int base = 0; base < total; base += 32) { // warp-uniform
-        const int q = base + lane;
-        const bool have = q < total;
-        // owning ray: the largest j with roff_j <= q (shuffle binary search over the warp's rays;
-        // a ray without runs has the same roff as the next ray that has some, which is larger)
-        int j = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const int c = j + step;
-            const int v = __shfl_sync(0xffffffffu, roff, c & 31);
-            j = (c < 32 && v <= q) ? c : j;
-        }
-        const long long roff_j = __shfl_sync(0xffffffffu, roff, j);
-        const int nr_j = __shfl_sync(0xffffffffu, nr, j);
-        const long long off_j = __shfl_sync(0xffffffffu, off, j);
-        const int fill_j = __shfl_sync(0xffffffffu, fill, j);
-        double first = 0.0;
-        long long g0 = 0;
-        int cnt = 0;
-        uint32_t cell = 0;
-        uint8_t lv = 0;
-        int32_t ri = 0;
-        if (have) {
-            const int local = q - (int)roff_j;
-            const RunRec* rec = S.runs + (r0 + j) * S.C + local;
-            const RunRec a = *rec;
-            const int start = (int)(a.sl & kRunStartMax);
-            const int end = local + 1 < nr_j ? (int)(rec[1].sl & kRunStartMax) : fill_j;
-            first = a.first;
-            g0 = off_j + start;
-            cnt = end - start;
-            cell = a.cell;
-            lv = (uint8_t)(a.sl >> 24);
-            ri = (int32_t)(ray_index_base + r0 + j);
-        }
-        const int last = min(total - base, 32) - 1;
-        const long long P0 = __shfl_sync(0xffffffffu, g0, 0);
-        const long long P1 = __shfl_sync(0xffffffffu, g0 + cnt, last);
-        for (long long w = P0; w < P1; w += kWarpW) { // warp-uniform windows
-            const long long we = (P1 - w < kWarpW) ? P1 : w + kWarpW;
-            if (cnt > 0 && cnt <= kShort && g0 < we && g0 + cnt > w) {
-                double t = first;
-                for (int k = 0; k < cnt; ++k) {
-                    const long long g = g0 + k;
-                    if (g >= we) break;
-                    if (g >= w) {
-                        const int p = (int)(g - w);
-                        wt[p] = t;
-                        wri[p] = ri;
-                        wce[p] = cell;
-                        wlv[p] = lv;
-                    }
-                    t = t + ladder_step<SCH>(t, s.dt0, s.growth);
-                }
-            }
-            unsigned lm = __ballot_sync(0xffffffffu, cnt > kShort && g0 < we && g0 + cnt > w);
-            while (lm) {
-                const int src = __ffs(lm) - 1;
-                lm &= lm - 1;
-                const double f = __shfl_sync(0xffffffffu, first, src);
-                const long long gb = __shfl_sync(0xffffffffu, g0, src);
-                const int nn = __shfl_sync(0xffffffffu, cnt, src);
-                const uint32_t ce = __shfl_sync(0xffffffffu, cell, src);
-                const int lvl = __shfl_sync(0xffffffffu, (int)lv, src);
-                const int32_t rr = __shfl_sync(0xffffffffu, ri, src);
-                double t1 = 0.0;
-                int64_t b2 = 0, inc = 0, kfast = 1;
-                if (SCH == 0) { // closed form after two explicit in-binade steps (sogk_ladder.cuh)
-                    t1 = f + s.dt0;
-                    const double t2 = t1 + s.dt0;
-                    const int64_t b0 = dbits(f), b1 = dbits(t1);
-                    b2 = dbits(t2);
-                    inc = b2 - b1;
-                    const int64_t e0 = b0 >> 52;
-                    if (e0 == (b2 >> 52) && e0 != 0 && inc > 0) {
-                        const int64_t end = (e0 + 1) << 52;
-                        kfast = 2 + fix_quotient(end - 1 - b2, inc, (dfrom(end) - t2) * s.inv_dt0);
-                    }
-                }
-                const int ka = (int)(w > gb ? w - gb : 0);
-                const int kb = (int)(gb + nn < we ? nn : we - gb);
-                for (int k = ka + lane; k < kb; k += 32) {
-                    double t;
-                    if (SCH == 0 && k <= kfast)
-                        t = k == 0 ? f : (k == 1 ? t1 : dfrom(b2 + (int64_t)(k - 2) * inc));
-                    else
-                        t = ladder_advance<SCH>(f, k, s.dt0, s.inv_dt0, s.growth, s.t_switch);
-                    const int p = (int)(gb + k - w);
-                    wt[p] = t;
-                    wri[p] = rr;
-                    wce[p] = ce;
-                    wlv[p] = (uint8_t)lvl;
-                }
-            }
-            __syncwarp();
-            const int m = (int)(we - w);
-            for (int p = lane; p < m; p += 32) { // coalesced: consecutive lanes, consecutive samples
-                const long long g = w + p;
-                const double t = wt[p];
-                __stcs(o.t_starts + g, t);
-                if (o.t_ends) __stcs(o.t_ends + g, t + ladder_step<SCH>(t, s.dt0, s.growth));
-                if (o.ray_indices) __stcs(o.ray_indices + g, wri[p]);
-                if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + g, wce[p]);
-                if (o.levels) o.levels[g] = wlv[p];
-            }
-            __syncwarp();
-        }
-    }
-}
-
 // pass 2 for the rays whose slab overflowed: resume the traversal at the first run that
 // did not fit and write the rest of the ray directly
 template <int AN, bool CASC, bool BR, int SCH, bool VEC, class Src>
@@ -1000,9 +848,7 @@ struct Launch {
             return cudaGetLastError();
         }
         const unsigned gb = (unsigned)((n + kGather - 1) / kGather);
-        if (SOGK_GATHER_WARP)
-            gather_warp_kernel<SCH><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
-        else if (vec && SOGK_GATHER_VEC)
+        if (vec && SOGK_GATHER_VEC)
             gather_kernel<SCH, true><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
         else
             gather_kernel<SCH, false><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
