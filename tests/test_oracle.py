@@ -238,3 +238,42 @@ def test_oracle_vs_reference_randomized(oracle, reflib, P):
                     assert np.array_equal(o.packed_info, r.packed_info)
                     assert _eq64(o.t_starts, r.t_starts) and _eq64(o.t_ends, r.t_ends)
                     assert np.array_equal(o.cells, r.cells) and np.array_equal(o.counters, r.counters)
+
+
+def test_oracle_vs_reference_config_shapes(oracle, reflib, P):
+    """The oracle pinned to the unmodified reference at the benchmark configurations' shapes
+    (CPU, sub-sampled rays): 128^3 scenes of cfg2 on orbit-camera rays, the 4-level cfg3 cascade
+    at 1297x840 (linear schedule, the spinning u == 0 column included and screened), and 512^3
+    blobs with make_probe_rays (cfg4) -- every variant, outputs and counters bit for bit."""
+    from oracle_bindings import CD
+
+    def same(o, r, what):
+        ok = o.status != 2
+        assert np.array_equal(o.packed_info[ok, 1], r.packed_info[ok, 1]), what
+        assert _eq64(o.t_starts, r.t_starts) and _eq64(o.t_ends, r.t_ends), what
+        assert np.array_equal(o.cells, r.cells) and np.array_equal(o.levels, r.levels), what
+        assert np.array_equal(o.counters[ok], r.counters[ok]), what
+
+    cam = reflib.camera_rays((2.9, 1.4, -1.3), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, 800, 800)[::211]
+    for kind, kw in (("shell", dict(seed=2, count=256)), ("blobs", dict(seed=3, count=24)),
+                     ("sponge", dict(seed=1)), ("random", dict(seed=1, fraction=0.02))):
+        g = reflib.scene(kind, 128, seed=kw["seed"], fraction=kw.get("fraction", 0.05), count=kw.get("count", 12))
+        for an in (DDA, HDDA, CD):
+            for k in (BRANCH, SKIP):
+                o = oracle.sample(oracle.sampler([g], an, k, CONSTANT, 0.5 * g.voxel), cam)
+                r = reflib.sampler([g], an, k, CONSTANT, 0.5 * g.voxel).sample(cam, skip=(o.status == 2))
+                same(o, r, f"{kind} an={an} k={k}")
+    lv = reflib.cascade("blobs", 4, 128, seed=1)
+    rays = reflib.camera_rays((1.9, 1.4, 2.3), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 42.0, 1297, 840)
+    sub = np.concatenate([rays[::97], rays[648::1297]])  # a strided sample + the u == 0 column
+    for an in (DDA, HDDA):
+        o = oracle.sample(oracle.sampler(lv, an, SKIP, LINEAR, 0.5 * lv[0].voxel, 1.0 / 256, cascade=True), sub)
+        r = reflib.sampler(lv, an, SKIP, LINEAR, 0.5 * lv[0].voxel, 1.0 / 256, cascade=True).sample(
+            sub, skip=(o.status == 2))
+        same(o, r, f"cascade an={an}")
+    g = reflib.scene("blobs", 512, seed=1)
+    probe = reflib.probe_rays(g, 3000, 1000)
+    for an in (DDA, HDDA):
+        o = oracle.sample(oracle.sampler([g], an, SKIP, CONSTANT, 0.5 * g.voxel), probe)
+        r = reflib.sampler([g], an, SKIP, CONSTANT, 0.5 * g.voxel).sample(probe, skip=(o.status == 2))
+        same(o, r, f"512^3 an={an}")
