@@ -1202,9 +1202,36 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     uint32_t* perm = nullptr;
     if (s->ray_order && !cam)
         CK(launch_ray_binning(s->dev, d_rays, n, s->bin_scratch(w, n), &perm, S(stream)), "ray binning");
+    // SOGK_L2_PERSIST=1 (experiment; measured no gain): pass 1 of a single VDB runs
+    // with an L2 persisting access-policy window over its child tables + leaves' first MBs
+    static const bool l2p = std::getenv("SOGK_L2_PERSIST") != nullptr;
+    const sogk_grid* g0 = s->lv[0];
+    const bool persist = l2p && s->n_levels == 1 && g0 && g0->kind == SOGK_GRID_VDB;
+    if (persist) {
+        static std::once_flag once;
+        std::call_once(once, [] {
+            int dev = 0, mx = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            if (mx > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(mx));
+            cudaGetLastError();
+        });
+        cudaStreamAttrValue av{};
+        av.accessPolicyWindow.base_ptr = g0->table;
+        av.accessPolicyWindow.num_bytes = size_t(g0->nreg) * 4096 * sizeof(int32_t);
+        av.accessPolicyWindow.hitRatio = 1.0f;
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        CK(cudaStreamSetAttribute(S(stream), cudaStreamAttributeAccessPolicyWindow, &av), "L2 window");
+    }
     CK(launch_count(s->v, s->dev, d_rays, cam ? &cd : nullptr, first, n, d_packed, d_stats,
                     d_status, d_counters, slab, S(stream), perm),
        "count launch");
+    if (persist) { // restore the caller's stream
+        cudaStreamAttrValue av{};
+        av.accessPolicyWindow.num_bytes = 0;
+        CK(cudaStreamSetAttribute(S(stream), cudaStreamAttributeAccessPolicyWindow, &av), "L2 window");
+    }
     CK(launch_scan(n, d_packed, d_stats, sogk_sampler::tiles(w),
                    reinterpret_cast<unsigned int*>(sogk_sampler::tiles(w) + tiles), S(stream)),
        "scan launch");
