@@ -410,9 +410,6 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
 #ifndef SOGK_HDDA_SMEM
 #define SOGK_HDDA_SMEM 1
 #endif
-#ifndef SOGK_REDERIVE2
-#define SOGK_REDERIVE2 0 // 1: re-derive only the two non-stepped axes (A/B)
-#endif
 // Kernels using the node analyzers or the cascade launch 1-D blocks of at most kGeomBlock
 // threads (per-thread shared-memory columns).
 constexpr int kGeomBlock = 128;
@@ -551,24 +548,11 @@ struct NodeAn {
         // cell_after_crossing (:91-104) at t_cur (degenerate) or t1, all axes
         // evaluated and the stepped one overridden
         const double dt = (degen ? t_cur : t1) - te;
-#if SOGK_REDERIVE2
-        {
-            // only the two axes that were not stepped are re-derived (the stepped one is set to the
-            // cell past its plane): two DMUL + DADD + F2I instead of three -- pass 1 is FP64-pipe
-            // throttled -- at the cost of integer selects and indexed shared-memory loads
-            const int b0 = axis == 0 ? 1 : 0, b1 = axis == 2 ? 1 : 2;
-            const int c0 = __double2int_rd(E(b0) + dt * DV(b0)) ^ M(b0);
-            const int c1 = __double2int_rd(E(b1) + dt * DV(b1)) ^ M(b1);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) ijk[a] = (a == axis) ? (pl[a] ^ M(a)) : (a == b0 ? c0 : c1);
-        }
-#else
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const int c = __double2int_rd(E(a) + dt * DV(a)) ^ M(a);
             ijk[a] = (a == axis) ? (pl[a] ^ M(a)) : c;
         }
-#endif
         if (degen) {
             // the reference spins forever at exact edge crossings
             if (++degenerate > spin_cap) {
