@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -1780,8 +1781,12 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     // host expansion of t_ends / ray_indices, chunk by chunk as their downloads finish
     const double dt0 = s->dev.dt0, growth = s->dev.growth;
     const bool linear = s->v.linear != 0;
-    std::atomic<int64_t> issued{0};   // chunks whose write + downloads are issued
-    std::atomic<bool> abort_exp{false};
+    // chunks whose write + downloads are issued (the expander sleeps on the condition variable
+    // until the next one is, then on that chunk's download event: no spinning host thread)
+    int64_t issued = 0;
+    bool abort_exp = false;
+    std::mutex exp_mu;
+    std::condition_variable exp_cv;
     auto expand_chunk = [&](int64_t c) {
         const int64_t r0 = c * chunk, m = std::min(chunk, n - r0);
         auto work = [&](int64_t a, int64_t b) { // rays [a, b) of the chunk
@@ -1821,8 +1826,11 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
     if (expand && nchunks > 0) {
         expander = std::thread([&] {
             for (int64_t c = 0; c < nchunks; ++c) {
-                while (issued.load() <= c && !abort_exp.load()) std::this_thread::yield();
-                if (abort_exp.load()) return;
+                {
+                    std::unique_lock<std::mutex> lk(exp_mu);
+                    exp_cv.wait(lk, [&] { return issued > c || abort_exp; });
+                    if (abort_exp) return;
+                }
                 if (cudaEventSynchronize(s->done_ev[c]) != cudaSuccess) return;
                 if (chunk_base[size_t(c)] >= 0) expand_chunk(c);
             }
@@ -1874,7 +1882,11 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         if (h_status) CK(cudaMemcpyAsync(h_status + r0, d_status + r0, size_t(m), cudaMemcpyDeviceToHost, L), "D2H");
         if (h_counters) CK(cudaMemcpyAsync(h_counters + 3 * r0, d_ctr + 3 * r0, size_t(m) * 12, cudaMemcpyDeviceToHost, L), "D2H");
         CK(cudaEventRecord(s->done_ev[c], L), "event");
-        issued.store(c + 1);
+        {
+            std::lock_guard<std::mutex> lk(exp_mu);
+            issued = c + 1;
+        }
+        exp_cv.notify_one();
         base += tot;
         return SOGK_OK;
     };
@@ -1883,7 +1895,13 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         if (rc == SOGK_OK && c > 0) rc = issue_write(c - 1);
         if (c + 1 == nchunks && rc == SOGK_OK) rc = issue_write(c);
     }
-    if (rc != SOGK_OK) abort_exp.store(true);
+    if (rc != SOGK_OK) {
+        {
+            std::lock_guard<std::mutex> lk(exp_mu);
+            abort_exp = true;
+        }
+        exp_cv.notify_one();
+    }
     for (int l = 0; l < kLanes; ++l) {
         const cudaError_t e = cudaStreamSynchronize(s->lanes[l]);
         if (e != cudaSuccess && rc == SOGK_OK) rc = cuda_fail(e, "pipeline sync");
