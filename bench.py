@@ -385,12 +385,12 @@ def run_gpu(args):
     }
     if args.variants:
         variants = {k: v for k, v in variants.items() if k in args.variants.split(",")}
-    samplers = {}
-    for vname, (an, kk) in variants.items():
-        samplers[vname] = [P.Sampler(grids[i][1] if an == P.Analyzer.hdda else
-                                     dist_grids[i] if an == P.Analyzer.cd else grids[i][0], an, kk,
-                                     sched, cascade=wl.cascade, ray_order=wl.ray_order)
-                           for i in range(n_obj)]
+    def make_sampler(vname, i):
+        an, kk = variants[vname]
+        return P.Sampler(grids[i][1] if an == P.Analyzer.hdda else dist_grids[i] if an == P.Analyzer.cd
+                         else grids[i][0], an, kk, sched, cascade=wl.cascade, ray_order=wl.ray_order)
+
+    samplers = {vname: [make_sampler(vname, i) for i in range(n_obj)] for vname in variants}
 
     steps_total = args.warmup + args.steps
     specs = [[wl.shard(s, o, rank, world) for o in range(n_obj)] for s in range(steps_total)]
@@ -616,16 +616,27 @@ def run_gpu(args):
                 t.copy_(rays[s][o], non_blocking=False)
                 row.append(t)
             h_rays.append(row)
-        hcap = max(obj_cap)
-        n_workers = max(1, min(args.e2e_workers, n_obj))
+        # units of host work: one object each (worker w takes objects w, w + W, ...), or, for a
+        # single-object config, the same contiguous ray ranges as the kernel legs' parts, one per
+        # worker with its own sampler (a sampler serialises its host calls)
+        if n_obj == 1 and args.e2e_workers > 1 and n_parts > 1:
+            units = [(make_sampler(vname0, 0) if pi else smp[0], 0, a, b,
+                      max(totals[(vname0, s_, pi)] for s_ in range(steps_total)))
+                     for pi, (_, a, b) in enumerate(parts)]
+            n_workers = len(units)
+        else:
+            units = [(smp[o], o, 0, nr, max(obj_cap)) for o in range(n_obj)]
+            n_workers = max(1, min(args.e2e_workers, n_obj))
+        hcap = max(1, max(u[4] for u in units))
+        urays = max(u[3] - u[2] for u in units)
 
         def host_outputs():  # pinned output buffers, one set per worker thread
-            o = dict(packed_info=torch.empty((nr, 2), dtype=torch.int64, pin_memory=True).numpy(),
+            o = dict(packed_info=torch.empty((urays, 2), dtype=torch.int64, pin_memory=True).numpy(),
                      t_starts=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
                      t_ends=torch.empty(hcap, dtype=torch.float64, pin_memory=True).numpy(),
                      ray_indices=torch.empty(hcap, dtype=torch.int32, pin_memory=True).numpy(),
                      stats=np.zeros(8, np.int64))
-            o["counters"] = torch.empty((nr, 3), dtype=torch.int32, pin_memory=True).numpy()
+            o["counters"] = torch.empty((urays, 3), dtype=torch.int32, pin_memory=True).numpy()
             return o
 
         h_outs = [host_outputs() for _ in range(n_workers)]
@@ -636,11 +647,12 @@ def run_gpu(args):
             # full: the north-star packed intervals (packed_info, t_starts, t_ends, ray_indices);
             # lean: what the reference's run_sampler returns per ray (sampling.hpp:157-164), its
             # sample buffer (packed t_starts + packed_info) and its three counters.  Worker w
-            # takes the objects o = w mod n_workers (independent samplers: each call is
-            # synchronous and pipelines its own chunks; ctypes drops the GIL, so calls overlap)
+            # takes units w, w + W, ... (independent samplers: each call is synchronous and
+            # pipelines its own chunks; ctypes drops the GIL, so calls overlap)
             h_out = h_outs[w]
-            for o in range(w, n_obj, n_workers):
-                rc = lib.sogk_sample_host(smp[o]._h, h_rays[s][o].data_ptr(), nr, base0, hcap,
+            for u in range(w, len(units), n_workers):
+                sm, o, a, b, cap_u = units[u]
+                rc = lib.sogk_sample_host(sm._h, h_rays[s][o].data_ptr() + a * 64, b - a, base0 + a, hcap,
                                           h_out["packed_info"].ctypes.data, h_out["t_starts"].ctypes.data,
                                           h_out["t_ends"].ctypes.data if full else None,
                                           h_out["ray_indices"].ctypes.data if full else None,
@@ -1013,7 +1025,7 @@ def main():
     ap.add_argument("--parity-stride", type=int, default=64,
                     help="every k-th ray of the first timed step is checked against the reference")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-workers", type=int, default=2,
+    ap.add_argument("--e2e-workers", type=int, default=4,
                     help="host threads issuing sogk_sample_host calls for different objects concurrently")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")

@@ -1708,7 +1708,7 @@ int sogk_sample_host(sogk_sampler* s, const double* h_rays, int64_t n, int64_t r
         const char* e = std::getenv("SOGK_HOST_THREADS");
         const long v = e ? std::atol(e) : 0;
         const int hw = int(std::thread::hardware_concurrency());
-        return int(v >= 1 && v <= 64 ? v : std::max(1, std::min(8, hw / 2)));
+        return int(v >= 1 && v <= 64 ? v : std::max(1, std::min(8, hw / 4)));
     }();
     const bool exp_ri = (kExpand & 1) && h_t_starts && h_ray_indices;
     const bool exp_te = (kExpand & 2) && h_t_starts && h_t_ends;
