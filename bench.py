@@ -1026,7 +1026,7 @@ def main():
                     help="every k-th ray of the first timed step is checked against the reference")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-workers", type=int, default=4,
-                    help="host threads issuing sogk_sample_host calls for different objects concurrently")
+                    help="host threads issuing sogk_sample_host calls concurrently (objects, or ray ranges of one object)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--streams", type=int, default=2,
