@@ -617,16 +617,26 @@ def run_gpu(args):
                 row.append(t)
             h_rays.append(row)
         # units of host work: one object each (worker w takes objects w, w + W, ...), or, for a
-        # single-object config, the same contiguous ray ranges as the kernel legs' parts, one per
-        # worker with its own sampler (a sampler serialises its host calls)
-        if n_obj == 1 and args.e2e_workers > 1 and n_parts > 1:
-            units = [(make_sampler(vname0, 0) if pi else smp[0], 0, a, b,
-                      max(totals[(vname0, s_, pi)] for s_ in range(steps_total)))
-                     for pi, (_, a, b) in enumerate(parts)]
-            n_workers = len(units)
+        # single-object config, one contiguous ray range per worker with its own sampler (a sampler
+        # serialises its host calls); capacities from an untimed count of every step
+        if n_obj == 1 and args.e2e_workers > 1:
+            W = args.e2e_workers
+            cut = [nr * i // W for i in range(W + 1)]
+            caps = [0] * W
+            pk = torch.empty((nr, 2), dtype=torch.int64, device=dev)
+            st_ = torch.zeros(8, dtype=torch.int64, device=dev)
+            for s_ in range(steps_total):  # per-range sample totals (untimed sizing)
+                smp[0].count(rays[s_][0], packed_info=pk, stats=st_)
+                cs = torch.cumsum(pk[:, 1], 0).cpu().numpy()
+                for i in range(W):
+                    tot_i = int(cs[cut[i + 1] - 1] - (cs[cut[i] - 1] if cut[i] > 0 else 0)) if cut[i + 1] > cut[i] else 0
+                    caps[i] = max(caps[i], tot_i)
+            units = [(make_sampler(vname0, 0) if i else smp[0], 0, cut[i], cut[i + 1], caps[i]) for i in range(W)]
+            n_workers = W
         else:
             units = [(smp[o], o, 0, nr, max(obj_cap)) for o in range(n_obj)]
             n_workers = max(1, min(args.e2e_workers, n_obj))
+        P.release_workspaces()
         hcap = max(1, max(u[4] for u in units))
         urays = max(u[3] - u[2] for u in units)
 
