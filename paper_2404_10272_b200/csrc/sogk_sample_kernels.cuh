@@ -164,21 +164,11 @@ __device__ __forceinline__ void count_invalid(long long r, int64_t* packed, uint
 // ---------------------------------------------------------------------------
 // pass 1: per-ray counts, status, counters, slab samples, resume state
 // ---------------------------------------------------------------------------
+// one ray of pass 1 (the ray the j-th processing slot names: src.id(j))
 template <int AN, bool CASC, bool BR, int SCH, class Src>
-__global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MINB)
-    count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
-                 int64_t* __restrict__ stats, uint8_t* __restrict__ status,
-                 int32_t* __restrict__ counters, const SlabDev S) {
-    if (s.lv[0].smem_tab) { // stage the single-region child table (16 KB) in shared memory
-        const int32_t node0 = __ldg(s.lv[0].root);
-        const int4* tsrc = reinterpret_cast<const int4*>(s.lv[0].table + (int64_t)(node0 < 0 ? 0 : node0) * 4096);
-        int4* tdst = reinterpret_cast<int4*>(sogk_dyn_smem);
-        for (int i = threadIdx.x; i < 1024; i += kBlock) tdst[i] = __ldg(tsrc + i);
-        __syncthreads();
-    }
-    const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    Stats5 acc;
-    if (j < n) {
+__device__ __forceinline__ void count_one(const SamplerDev& s, const Src& src, int64_t j, int64_t* __restrict__ packed,
+                                          uint8_t* __restrict__ status, int32_t* __restrict__ counters,
+                                          const SlabDev& S, Stats5& acc) {
         const int64_t r = src.id(j);
         const Ray ray = src.load(r);
         if (!ray_valid(ray)) {
@@ -231,7 +221,23 @@ __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MIN
                 ++acc.ovf;
             }
         }
+}
+
+template <int AN, bool CASC, bool BR, int SCH, class Src>
+__global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MINB)
+    count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
+                 int64_t* __restrict__ stats, uint8_t* __restrict__ status,
+                 int32_t* __restrict__ counters, const SlabDev S) {
+    if (s.lv[0].smem_tab) { // stage the single-region child table (16 KB) in shared memory
+        const int32_t node0 = __ldg(s.lv[0].root);
+        const int4* tsrc = reinterpret_cast<const int4*>(s.lv[0].table + (int64_t)(node0 < 0 ? 0 : node0) * 4096);
+        int4* tdst = reinterpret_cast<int4*>(sogk_dyn_smem);
+        for (int i = threadIdx.x; i < 1024; i += kBlock) tdst[i] = __ldg(tsrc + i);
+        __syncthreads();
     }
+    Stats5 acc;
+    const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (j < n) count_one<AN, CASC, BR, SCH, Src>(s, src, j, packed, status, counters, S, acc);
     acc.flush(stats); // warp-level: no block barrier, finished warps leave at once
 }
 
@@ -737,8 +743,9 @@ struct Launch {
             s2.lv[0].smem_tab = 1;
             dyn = 4096 * sizeof(int32_t);
         }
+        const unsigned grid = (unsigned)blocks;
         count_kernel<AN, CASC, BR, SCH, Src>
-            <<<(unsigned)blocks, kBlock, dyn, st>>>(s2, src, n, packed, stats, status, counters, S);
+            <<<grid, kBlock, dyn, st>>>(s2, src, n, packed, stats, status, counters, S);
         return cudaGetLastError();
     }
     template <int AN, bool CASC, bool BR, int SCH>

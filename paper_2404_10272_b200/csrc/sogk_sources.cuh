@@ -1,4 +1,4 @@
-// sogk_sources.cuh — ray sources of the sampling kernels and the variant dispatch.
+// sogk_sources.cuh — ray sources of the sampling kernels and the analyzer selection.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -67,36 +67,5 @@ struct PickAn {
         AN == SOGK_HDDA, HddaAn, typename std::conditional<AN == SOGK_CD, CdAn, DdaAn>::type>::type;
     using type = AnyAn<Sub, CASC>;
 };
-
-#define SOGK_DISPATCH(FN, ...)                                                                    \
-    do {                                                                                          \
-        const int key = (v.analyzer << 3) | (v.cascade << 2) | (v.branch << 1) | v.linear;       \
-        switch (key) {                                                                            \
-            case 0: return L::template FN<0, false, false, 0>(__VA_ARGS__);                       \
-            case 1: return L::template FN<0, false, false, 1>(__VA_ARGS__);                       \
-            case 2: return L::template FN<0, false, true, 0>(__VA_ARGS__);                        \
-            case 3: return L::template FN<0, false, true, 1>(__VA_ARGS__);                        \
-            case 4: return L::template FN<0, true, false, 0>(__VA_ARGS__);                        \
-            case 5: return L::template FN<0, true, false, 1>(__VA_ARGS__);                        \
-            case 6: return L::template FN<0, true, true, 0>(__VA_ARGS__);                         \
-            case 7: return L::template FN<0, true, true, 1>(__VA_ARGS__);                         \
-            case 8: return L::template FN<1, false, false, 0>(__VA_ARGS__);                       \
-            case 9: return L::template FN<1, false, false, 1>(__VA_ARGS__);                       \
-            case 10: return L::template FN<1, false, true, 0>(__VA_ARGS__);                       \
-            case 11: return L::template FN<1, false, true, 1>(__VA_ARGS__);                       \
-            case 12: return L::template FN<1, true, false, 0>(__VA_ARGS__);                       \
-            case 13: return L::template FN<1, true, false, 1>(__VA_ARGS__);                       \
-            case 14: return L::template FN<1, true, true, 0>(__VA_ARGS__);                        \
-            case 15: return L::template FN<1, true, true, 1>(__VA_ARGS__);                        \
-            case 16: return L::template FN<2, false, false, 0>(__VA_ARGS__);                      \
-            case 17: return L::template FN<2, false, false, 1>(__VA_ARGS__);                      \
-            case 18: return L::template FN<2, false, true, 0>(__VA_ARGS__);                       \
-            case 19: return L::template FN<2, false, true, 1>(__VA_ARGS__);                       \
-            case 20: return L::template FN<2, true, false, 0>(__VA_ARGS__);                       \
-            case 21: return L::template FN<2, true, false, 1>(__VA_ARGS__);                       \
-            case 22: return L::template FN<2, true, true, 0>(__VA_ARGS__);                        \
-            default: return L::template FN<2, true, true, 1>(__VA_ARGS__);                        \
-        }                                                                                         \
-    } while (0)
 
 } // namespace sogk
