@@ -406,11 +406,13 @@ def run_gpu(args):
 
     # parts: the units one count/write pair processes -- one per object, or, for single-object
     # configs on several streams, one contiguous ray range per stream (each its own packed batch)
-    if n_obj == 1 and args.streams > 1:
-        cut = [nr * i // args.streams for i in range(args.streams + 1)]
-        parts = [(0, cut[i], cut[i + 1]) for i in range(args.streams)]
-    else:
-        parts = [(o, 0, nr) for o in range(n_obj)]
+    # (--chunk-rays caps a part's rays: its pass-1 run slabs then stay L2-resident until pass 2
+    # reads them, and the next chunk's pass 1 rewrites the same workspace lines in L2)
+    k_obj = args.streams if (n_obj == 1 and args.streams > 1) else 1
+    if args.chunk_rays > 0:
+        k_obj = max(k_obj, -(-nr // args.chunk_rays))
+    cut = [nr * i // k_obj for i in range(k_obj + 1)]
+    parts = [(o, cut[i], cut[i + 1]) for o in range(n_obj) for i in range(k_obj)]
     n_parts = len(parts)
 
     def prays(s_, pi):
@@ -1041,6 +1043,8 @@ def main():
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams the step's objects are spread over (1: one stream)")
+    ap.add_argument("--chunk-rays", type=int, default=0,
+                    help="at most this many rays per count/write pair (0: one pair per object or stream part)")
     ap.add_argument("--backend", default="nccl", help="torch.distributed backend under torchrun (tests: gloo)")
     ap.add_argument("--dump", default="", help="directory: every rank saves its outputs of the first timed step")
     args = ap.parse_args()
