@@ -556,7 +556,11 @@ class Sampler:
         sh = _stream(stream)
         _check(lib.sogk_sample_count_ex(self._h, _ptr(rays), n, _ptr(packed), _ptr(st), _ptr(status),
                                         _ptr(counters), sh, C.byref(tok)), "sample_count")
-        self._tokens[_ptr(packed)] = (tok.value, _ptr(rays), n)
+        key = _ptr(packed)
+        self._tokens.pop(key, None)
+        self._tokens[key] = (tok.value, _ptr(rays), n)
+        while len(self._tokens) > 64:  # only the latest counts can still own a workspace
+            self._tokens.pop(next(iter(self._tokens)))
         return packed, st
 
     def write(self, rays, packed_info, total: int, ray_index_base: int = 0, stream=None,
