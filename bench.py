@@ -489,10 +489,16 @@ def run_gpu(args):
             # the next object's pass 1 (issue-bound); sizes are precomputed, no host sync
             side = [torch.cuda.Stream(device=dev) for _ in range(args.streams)]
 
-            def step_overlapped(s):
+            first_count = torch.cuda.Event()
+
+            def step_overlapped(s, offset=False):
                 for pi, (o, a, b) in enumerate(parts):
                     st = side[pi % args.streams]
+                    if offset and 0 < pi < args.streams:
+                        st.wait_event(first_count)  # start half a pass later (--stagger)
                     smp[o].count(prays(s, pi), packed_info=packed[pi], stats=stats[pi], stream=st)
+                    if offset and pi == 0:
+                        first_count.record(st)
                     smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=base0 + a,
                                  out=outs[pi], cells=True, levels=False, stream=st)
 
@@ -512,7 +518,10 @@ def run_gpu(args):
                 for st in side:
                     st.wait_event(u0)
                 for k in range(args.steps):
-                    step_overlapped(args.warmup + k)
+                    # --stagger 1: the second stream starts after the first stream's first pass 1 of
+                    # the timed region, so one stream's pass 2 overlaps the other's pass 1;
+                    # 2: the same at every step
+                    step_overlapped(args.warmup + k, offset=(args.stagger == 1 and k == 0) or args.stagger == 2)
                 for st in side:
                     stream.wait_stream(st)
                 u1.record(stream)
@@ -1043,6 +1052,8 @@ def main():
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams the step's objects are spread over (1: one stream)")
+    ap.add_argument("--stagger", type=int, default=0, choices=[0, 1, 2],
+                    help="offset the second stream by one pass 1 (1: at the start, 2: every step)")
     ap.add_argument("--chunk-rays", type=int, default=0,
                     help="at most this many rays per count/write pair (0: one pair per object or stream part)")
     ap.add_argument("--backend", default="nccl", help="torch.distributed backend under torchrun (tests: gloo)")
