@@ -489,16 +489,23 @@ def run_gpu(args):
             # the next object's pass 1 (issue-bound); sizes are precomputed, no host sync
             side = [torch.cuda.Stream(device=dev) for _ in range(args.streams)]
 
-            first_count = torch.cuda.Event()
+            # parts -> streams: longest-processing-time first over the one-stream leg's per-part
+            # times, so the streams' loads are even (objects differ ~4x in cost)
+            part_ms = [sum(evs[k][pi][0].elapsed_time(evs[k][pi][2]) for k in range(args.steps))
+                       for pi in range(n_parts)]
+            load = [0.0] * args.streams
+            assign = [0] * n_parts
+            for pi in sorted(range(n_parts), key=lambda i: -part_ms[i]):
+                j = min(range(args.streams), key=lambda x: load[x])
+                assign[pi] = j
+                load[j] += part_ms[pi]
+            if not args.balance:
+                assign = [pi % args.streams for pi in range(n_parts)]
 
-            def step_overlapped(s, offset=False):
+            def step_overlapped(s):
                 for pi, (o, a, b) in enumerate(parts):
-                    st = side[pi % args.streams]
-                    if offset and 0 < pi < args.streams:
-                        st.wait_event(first_count)  # start half a pass later (--stagger)
+                    st = side[assign[pi]]
                     smp[o].count(prays(s, pi), packed_info=packed[pi], stats=stats[pi], stream=st)
-                    if offset and pi == 0:
-                        first_count.record(st)
                     smp[o].write(prays(s, pi), packed[pi], totals[(vname, s, pi)], ray_index_base=base0 + a,
                                  out=outs[pi], cells=True, levels=False, stream=st)
 
@@ -518,10 +525,7 @@ def run_gpu(args):
                 for st in side:
                     st.wait_event(u0)
                 for k in range(args.steps):
-                    # --stagger 1: the second stream starts after the first stream's first pass 1 of
-                    # the timed region, so one stream's pass 2 overlaps the other's pass 1;
-                    # 2: the same at every step
-                    step_overlapped(args.warmup + k, offset=(args.stagger == 1 and k == 0) or args.stagger == 2)
+                    step_overlapped(args.warmup + k)
                 for st in side:
                     stream.wait_stream(st)
                 u1.record(stream)
@@ -1052,8 +1056,8 @@ def main():
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams the step's objects are spread over (1: one stream)")
-    ap.add_argument("--stagger", type=int, default=0, choices=[0, 1, 2],
-                    help="offset the second stream by one pass 1 (1: at the start, 2: every step)")
+    ap.add_argument("--balance", type=int, default=1,
+                    help="1: assign parts to streams by measured cost (LPT); 0: round robin")
     ap.add_argument("--chunk-rays", type=int, default=0,
                     help="at most this many rays per count/write pair (0: one pair per object or stream part)")
     ap.add_argument("--backend", default="nccl", help="torch.distributed backend under torchrun (tests: gloo)")
