@@ -1056,7 +1056,7 @@ def main():
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams the step's objects are spread over (1: one stream)")
-    ap.add_argument("--balance", type=int, default=1,
+    ap.add_argument("--balance", type=int, default=0,
                     help="1: assign parts to streams by measured cost (LPT); 0: round robin")
     ap.add_argument("--chunk-rays", type=int, default=0,
                     help="at most this many rays per count/write pair (0: one pair per object or stream part)")
