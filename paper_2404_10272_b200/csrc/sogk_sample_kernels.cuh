@@ -18,7 +18,7 @@ constexpr int kWriteBlock = 128;
 #define SOGK_GATHER_SHORT 8
 #endif
 #ifndef SOGK_CASC_MINB
-#define SOGK_CASC_MINB 1 // the same for the cascade variants
+#define SOGK_CASC_MINB 5 // cascade variants: <= 96 registers (A/B cfg3: HDDA step -4 %, DDA -24 % vs 126)
 #endif
 #ifndef SOGK_COUNT_MINB
 #define SOGK_COUNT_MINB 7 // pass-1 min resident blocks per SM: <= 72 registers (A/B: -2 % HDDA, -7 % DDA vs 76-88)
