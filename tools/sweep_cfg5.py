@@ -37,7 +37,21 @@ def timed(fn, reps):
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
+    timed.last = times
     return sorted(times)[len(times) // 2], outs[-1]
+
+
+def split_ms(s, r, packed, total, outs):
+    """One more launch with events around each pass: (count incl. scan, write) ms."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    s.count(r, packed_info=packed)
+    ev[1].record()
+    s.write(r, packed, total, out=outs)
+    ev[2].record()
+    torch.cuda.synchronize()
+    return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
 
 
 def main():
@@ -98,6 +112,9 @@ def main():
                     launch()
                     ms, tot = timed(launch, a.reps)
                     assert tot == total
+                    row["rep_ms"] = timed.last
+                    row["count_ms"], row["write_ms"] = split_ms(s, r, packed, total, outs)
+                    row["free_gb"] = torch.cuda.mem_get_info()[0] / 1e9
                     _, stt = s.count(r, packed_info=packed)
                     row["slab_overflow_rays"] = int(stt.cpu()[P.STAT_SLAB_OVERFLOW_RAYS])
                     row.update(status="ok", ms=ms, rays_per_s=n / ms * 1e3, samples_per_s=total / ms * 1e3,
@@ -105,7 +122,9 @@ def main():
                     rows.append(row)
                     del outs
                     print(f"{family:6s} f={f:<6} occ={occ:.4f} {name:18s} n=2^{lg} {ms:9.3f} ms "
-                          f"{n / ms / 1e3:9.1f} Mrays/s {total / ms / 1e6:8.2f} Gsamples/s", flush=True)
+                          f"{n / ms / 1e3:9.1f} Mrays/s {total / ms / 1e6:8.2f} Gsamples/s  count {row['count_ms']:.2f} "
+                          f"write {row['write_ms']:.2f} ms  reps {[round(x, 2) for x in row['rep_ms']]} "
+                          f"overflow {row['slab_overflow_rays']} free {row['free_gb']:.0f} GB", flush=True)
             del variants, sparse, dense
             P.release_workspaces()
     json.dump({"config": "cfg5", "res": a.res, "dt0": 0.5 * t.voxel_size, "rows": rows},
