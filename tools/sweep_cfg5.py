@@ -59,7 +59,7 @@ def main():
     ap.add_argument("--res", type=int, default=128)
     ap.add_argument("--log2-min", type=int, default=20)
     ap.add_argument("--log2-max", type=int, default=26)
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out-cap-gb", type=float, default=48.0)
     ap.add_argument("--out", default="gpurun_out/cfg5")
     ap.add_argument("--fractions", default=",".join(str(f) for f in FRACTIONS))
