@@ -392,10 +392,107 @@ constexpr int kStageW = SOGK_STAGE_W;
 #define SOGK_GATHER_VEC 0 // 1: 128-bit stores of four samples per thread (A/B: pass 2 +11 % time, off)
 #endif
 
+// Output-parallel expansion of one pass-2 batch (constant schedule).  Per-run expansion
+// (gather_kernel's staged path) gives each long run to one lane, or one warp, while the rest
+// of the block waits at the window barrier; a batch with many long tile runs is expanded by
+// OUTPUT position instead.  Thread i decodes run i into the shared run table -- output start,
+// length, cell, level, ray index and the closed-form ladder constants of its first point
+// (t1 = f + dt0, then bits(t2) + (k - 2) * inc while in f's binade, sogk_ladder.cuh) -- and
+// then writes positions P0 + i, P0 + i + kGather, ... of the batch span: a branch-free binary
+// search over the run starts finds the owning run and point k comes from the closed form
+// (exact: the points of the reference recurrence t <- t + dt0, sampling.hpp:115-118).
+// Consecutive threads store consecutive samples of every array.  Positions no run covers
+// (the tails of slab-overflow rays) are skipped; tail_kernel writes them.
+#ifndef SOGK_GATHER_MP
+#define SOGK_GATHER_MP 32 // output-parallel when >= 1/32 of a batch's runs are long; 0: never
+#endif
+#ifndef SOGK_MP_NARROW
+#define SOGK_MP_NARROW 1 // search 32-bit span-relative run starts when the span allows
+#endif
+struct MpTab {
+    long long g0[kGather]; // output start (LLONG_MAX past the batch)
+    int rel[kGather];      // g0 - P0 for spans below 2^31 (INT_MAX past the batch)
+    double f[kGather], t1[kGather];
+    long long b2[kGather], inc[kGather];
+    int n[kGather], kf[kGather];
+    uint32_t ce[kGather];
+    int32_t ri[kGather];
+    uint8_t lv[kGather];
+};
+
+__device__ __forceinline__ void gather_mp_batch(const SamplerDev& s, const Out& o, MpTab& T, bool have,
+                                                double f, long long g0, int nn, uint32_t cell, uint8_t lv,
+                                                int32_t ri, long long P0, long long P1) {
+    const int tid = threadIdx.x;
+    const double dt0 = s.dt0;
+    const bool narrow = SOGK_MP_NARROW && P1 - P0 < (long long)INT_MAX; // block-uniform
+    if (have) {
+        T.g0[tid] = g0;
+        T.rel[tid] = narrow ? (int)(g0 - P0) : 0;
+        T.n[tid] = nn;
+        T.f[tid] = f;
+        T.ce[tid] = cell;
+        T.lv[tid] = lv;
+        T.ri[tid] = ri;
+        const double t1 = f + dt0;
+        T.t1[tid] = t1;
+        int kf = 1;
+        if (nn > 2) { // closed form after two explicit in-binade steps
+            const double t2 = t1 + dt0;
+            const int64_t b0 = dbits(f), b1 = dbits(t1), b2 = dbits(t2);
+            const int64_t inc = b2 - b1;
+            const int64_t e0 = b0 >> 52;
+            if (e0 == (b2 >> 52) && e0 != 0 && inc > 0) {
+                const int64_t endb = (e0 + 1) << 52;
+                const int64_t kq = 2 + fix_quotient(endb - 1 - b2, inc, (dfrom(endb) - t2) * s.inv_dt0);
+                kf = kq < nn ? (int)kq : nn;
+            }
+            T.b2[tid] = b2;
+            T.inc[tid] = inc;
+        }
+        T.kf[tid] = kf;
+    } else {
+        T.g0[tid] = LLONG_MAX;
+        T.rel[tid] = INT_MAX;
+    }
+    __syncthreads();
+    for (long long p = P0 + tid; p < P1; p += kGather) {
+        int j = 0; // the last run starting at or before p
+        if (narrow) {
+            const int rp = (int)(p - P0);
+#pragma unroll
+            for (int step = kGather / 2; step > 0; step >>= 1)
+                j += (T.rel[j + step] <= rp) ? step : 0;
+        } else {
+#pragma unroll
+            for (int step = kGather / 2; step > 0; step >>= 1)
+                j += (T.g0[j + step] <= p) ? step : 0;
+        }
+        const long long k = p - T.g0[j];
+        if (k < T.n[j]) {
+            double t;
+            if (k == 0)
+                t = T.f[j];
+            else if (k == 1)
+                t = T.t1[j];
+            else if (k <= T.kf[j])
+                t = dfrom(T.b2[j] + (k - 2) * T.inc[j]);
+            else
+                t = advance_const(T.f[j], k, dt0, s.inv_dt0);
+            __stcs(o.t_starts + p, t);
+            if (o.t_ends) __stcs(o.t_ends + p, t + dt0);
+            if (o.ray_indices) __stcs(o.ray_indices + p, T.ri[j]);
+            if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + p, T.ce[j]);
+            if (o.levels) o.levels[p] = T.lv[j];
+        }
+    }
+    __syncthreads();
+}
+
 #ifndef SOGK_GATHER_MINB
 #define SOGK_GATHER_MINB 4 // <= 64 registers: 4 blocks of 256 per SM
 #endif
-template <int SCH, bool VEC>
+template <int SCH, bool VEC, bool MP>
 __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
     gather_kernel(const __grid_constant__ SamplerDev s, int64_t n, const int64_t* __restrict__ packed,
                   const SlabDev S, int64_t ray_index_base, const Out o) {
@@ -450,11 +547,14 @@ __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
     // and every window goes out with fully coalesced stores (a warp writes 32 consecutive
     // samples of each array).  Positions no run covers (the tails of slab-overflow rays) carry
     // stale values; tail_kernel, next on the stream, overwrites them.
-    __shared__ double s_t[kStageW];
-    __shared__ int32_t s_ri[kStageW];
-    __shared__ uint32_t s_ce[kStageW];
-    __shared__ uint8_t s_lv[kStageW];
+    // (the same bytes hold an output-parallel batch's run table, MpTab, when that path runs)
+    __shared__ __align__(16) unsigned char s_raw[kStageW * 17];
+    double* const s_t = reinterpret_cast<double*>(s_raw);
+    int32_t* const s_ri = reinterpret_cast<int32_t*>(s_raw + 8 * kStageW);
+    uint32_t* const s_ce = reinterpret_cast<uint32_t*>(s_raw + 12 * kStageW);
+    uint8_t* const s_lv = s_raw + 16 * kStageW;
     __shared__ long long s_span[2];
+    static_assert(sizeof(MpTab) <= sizeof(s_raw), "run table must fit the staging window");
 #endif
     // run records of the next batch are loaded while the current one is expanded (software
     // pipelining: the scattered 16-byte record loads are the kernel's long-scoreboard stall)
@@ -500,7 +600,19 @@ __global__ void __launch_bounds__(kGather, SOGK_GATHER_MINB)
 #if SOGK_GATHER_STAGED
         if (tid == 0) s_span[0] = g0; // the batch's first run starts its span
         if (have && (q + 1 == total || tid + 1 == kGather)) s_span[1] = g0 + n;
-        __syncthreads();
+        if constexpr (MP) {
+            // batches with many long (tile) runs go output-parallel (the count rides on the
+            // span barrier)
+            const int nlong = __syncthreads_count(have && n > kShort);
+            const int nb = total - base < kGather ? total - base : kGather;
+            if (nlong * SOGK_GATHER_MP >= nb) { // block-uniform
+                gather_mp_batch(s, o, *reinterpret_cast<MpTab*>(s_raw), have, first, g0, n, cell, lv, ri,
+                                s_span[0], s_span[1]);
+                continue;
+            }
+        } else {
+            __syncthreads();
+        }
         const long long P0 = s_span[0], P1 = s_span[1];
         for (long long w = P0; w < P1; w += kStageW) { // block-uniform
             const long long we = (P1 - w < kStageW) ? P1 : w + kStageW;
@@ -761,10 +873,13 @@ struct Launch {
             return cudaGetLastError();
         }
         const unsigned gb = (unsigned)((n + kGather - 1) / kGather);
+        // output-parallel batches for the HDDA (tile runs, constant schedule); DDA and CD runs
+        // are single voxels (a few points), for which per-run expansion is cheaper
+        constexpr bool kMp = AN == SOGK_HDDA && SCH == 0 && SOGK_GATHER_MP > 0;
         if (vec && SOGK_GATHER_VEC)
-            gather_kernel<SCH, true><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
+            gather_kernel<SCH, true, kMp><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
         else
-            gather_kernel<SCH, false><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
+            gather_kernel<SCH, false, kMp><<<gb, kGather, 0, st>>>(s, n, packed, *S, base, o);
         const unsigned tg = tail_grid(n);
         if (vec)
             tail_kernel<AN, CASC, BR, SCH, true, Src><<<tg, kWriteBlock, 0, st>>>(s, src, packed, *S, base, o);
