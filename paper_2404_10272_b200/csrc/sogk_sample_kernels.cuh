@@ -409,9 +409,12 @@ constexpr int kStageW = SOGK_STAGE_W;
 #ifndef SOGK_MP_NARROW
 #define SOGK_MP_NARROW 1 // search 32-bit span-relative run starts when the span allows
 #endif
+#ifndef SOGK_MP_PAIRS
+#define SOGK_MP_PAIRS 1 // narrow spans: two adjacent positions per thread, one search, 2-wide stores
+#endif
 struct MpTab {
     long long g0[kGather]; // output start (LLONG_MAX past the batch)
-    int rel[kGather];      // g0 - P0 for spans below 2^31 (INT_MAX past the batch)
+    int rel[kGather + 1];  // g0 - P0 for spans below 2^31 (INT_MAX past the batch)
     double f[kGather], t1[kGather];
     long long b2[kGather], inc[kGather];
     int n[kGather], kf[kGather];
@@ -455,7 +458,74 @@ __device__ __forceinline__ void gather_mp_batch(const SamplerDev& s, const Out& 
         T.g0[tid] = LLONG_MAX;
         T.rel[tid] = INT_MAX;
     }
+    if (tid == 0) T.rel[kGather] = INT_MAX;
     __syncthreads();
+    // point k of run j: the closed form of the reference recurrence
+    auto point = [&](int j, long long k) -> double {
+        if (k == 0) return T.f[j];
+        if (k == 1) return T.t1[j];
+        if (k <= T.kf[j]) return dfrom(T.b2[j] + (k - 2) * T.inc[j]);
+        return advance_const(T.f[j], k, dt0, s.inv_dt0);
+    };
+    const bool pair_ok = SOGK_MP_PAIRS && narrow &&
+                         (((uintptr_t)o.t_starts | (uintptr_t)o.t_ends) & 15) == 0 &&
+                         (((uintptr_t)o.ray_indices | (uintptr_t)o.cells) & 7) == 0 &&
+                         ((uintptr_t)o.levels & 1) == 0;
+    if (pair_ok) {
+        // thread i takes the aligned pair (A, A + 1), A = (P0 & ~1) + 2 i + 2 kGather m: one
+        // search for the first position inside the span, the second position is the same
+        // run's next point (t + dt0, the recurrence itself) or the next run's first
+        const long long A0 = P0 & ~1ll;
+        const long long npairs = (P1 - A0 + 1) >> 1;
+        for (long long i = tid; i < npairs; i += kGather) {
+            const long long A = A0 + 2 * i;
+            const int r0 = (int)(A - P0); // -1 for a pair that starts before the span
+            const int re = r0 < 0 ? 0 : r0;
+            int j = 0;
+#pragma unroll
+            for (int step = kGather / 2; step > 0; step >>= 1)
+                j += (T.rel[j + step] <= re) ? step : 0;
+            const int k0 = re - T.rel[j];
+            const bool v0 = r0 >= 0 && k0 < T.n[j];
+            int j1 = j, k1 = k0;
+            if (r0 >= 0) {
+                if (T.rel[j + 1] <= r0 + 1) { // the next run starts at A + 1
+                    j1 = j + 1;
+                    k1 = 0;
+                } else {
+                    k1 = k0 + 1;
+                }
+            }
+            const bool v1 = A + 1 < P1 && k1 < T.n[j1];
+            const double t0 = v0 ? point(j, k0) : 0.0;
+            const double t1 = v1 ? ((v0 && j1 == j) ? t0 + dt0 : point(j1, k1)) : 0.0;
+            if (v0 && v1) {
+                __stcs(reinterpret_cast<double2*>(o.t_starts + A), make_double2(t0, t1));
+                if (o.t_ends) __stcs(reinterpret_cast<double2*>(o.t_ends + A), make_double2(t0 + dt0, t1 + dt0));
+                if (o.ray_indices) __stcs(reinterpret_cast<int2*>(o.ray_indices + A), make_int2(T.ri[j], T.ri[j1]));
+                if (o.cells) __stcs(reinterpret_cast<uint2*>(o.cells + A), make_uint2(T.ce[j], T.ce[j1]));
+                if (o.levels)
+                    *reinterpret_cast<uint16_t*>(o.levels + A) = (uint16_t)(T.lv[j] | ((uint32_t)T.lv[j1] << 8));
+            } else {
+                if (v0) {
+                    __stcs(o.t_starts + A, t0);
+                    if (o.t_ends) __stcs(o.t_ends + A, t0 + dt0);
+                    if (o.ray_indices) __stcs(o.ray_indices + A, T.ri[j]);
+                    if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + A, T.ce[j]);
+                    if (o.levels) o.levels[A] = T.lv[j];
+                }
+                if (v1) {
+                    __stcs(o.t_starts + A + 1, t1);
+                    if (o.t_ends) __stcs(o.t_ends + A + 1, t1 + dt0);
+                    if (o.ray_indices) __stcs(o.ray_indices + A + 1, T.ri[j1]);
+                    if (o.cells) __stcs(reinterpret_cast<unsigned int*>(o.cells) + A + 1, T.ce[j1]);
+                    if (o.levels) o.levels[A + 1] = T.lv[j1];
+                }
+            }
+        }
+        __syncthreads();
+        return;
+    }
     for (long long p = P0 + tid; p < P1; p += kGather) {
         int j = 0; // the last run starting at or before p
         if (narrow) {
@@ -470,15 +540,7 @@ __device__ __forceinline__ void gather_mp_batch(const SamplerDev& s, const Out& 
         }
         const long long k = p - T.g0[j];
         if (k < T.n[j]) {
-            double t;
-            if (k == 0)
-                t = T.f[j];
-            else if (k == 1)
-                t = T.t1[j];
-            else if (k <= T.kf[j])
-                t = dfrom(T.b2[j] + (k - 2) * T.inc[j]);
-            else
-                t = advance_const(T.f[j], k, dt0, s.inv_dt0);
+            const double t = point(j, k);
             __stcs(o.t_starts + p, t);
             if (o.t_ends) __stcs(o.t_ends + p, t + dt0);
             if (o.ray_indices) __stcs(o.ray_indices + p, T.ri[j]);
