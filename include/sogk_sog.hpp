@@ -14,6 +14,7 @@
 // sog::io_error for SOG0/SOG1 problems, std::runtime_error for device failures.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -244,6 +245,13 @@ public:
         return out;
     }
 
+    /// This rank's share of a ray batch that every rank holds (multi-GPU, one process per
+    /// GPU): the contiguous range shard_range(n, world, rank) sampled with global
+    /// ray_indices.  Concatenating the ranks' outputs in rank order (offsets shifted by the
+    /// earlier ranks' totals) gives sample_rays(rays), for any world size.
+    PackedSamples sample_shard(std::span<const Ray> rays, int world, int rank,
+                               void* stream = nullptr) const;
+
     /// run_sampler for one ray (drop-in; prefer sample_rays for throughput)
     SampleRun operator()(const Ray& ray) const { return sample_rays({&ray, 1}).run(0); }
 
@@ -272,6 +280,29 @@ private:
     }
     std::shared_ptr<sogk_sampler> s_;
 };
+
+/// Contiguous ray range [first, first + count) of `rank` among `world` ranks: ceil(n / world)
+/// rays per rank, the last ranks possibly short or empty.  The reference splits a frame into
+/// row chunks the same way (render_frame, bench.hpp:446-450: rows_per = ceil(height / n)), and
+/// its output does not depend on the split; rays are independent, so no collective follows.
+struct ShardRange {
+    std::int64_t first = 0, count = 0;
+};
+inline ShardRange shard_range(std::int64_t n, int world, int rank) {
+    if (world < 1 || rank < 0 || rank >= world || n < 0)
+        throw std::invalid_argument("shard_range: need 0 <= rank < world and n >= 0");
+    const std::int64_t per = (n + world - 1) / world;
+    ShardRange r;
+    r.first = std::min<std::int64_t>(n, per * rank);
+    r.count = std::min<std::int64_t>(n, r.first + per) - r.first;
+    return r;
+}
+
+inline PackedSamples Sampler::sample_shard(std::span<const Ray> rays, int world, int rank,
+                                           void* stream) const {
+    const ShardRange sr = shard_range(std::int64_t(rays.size()), world, rank);
+    return sample_rays(rays.subspan(std::size_t(sr.first), std::size_t(sr.count)), sr.first, stream);
+}
 
 /// run_sampler overloads (sampling.hpp:166-196) over device grids
 inline SampleRun run_sampler(const Ray& ray, const DeviceDenseGrid& g, KernelKind k,

@@ -65,6 +65,30 @@ int main() {
             }
             EXPECT(mism == 0, "%ld ray mismatches (kernel %d)", mism, int(k));
         }
+    // rank shards (multi-GPU row split): concatenated shards == the whole batch, global ray_indices
+    {
+        const gpu::Sampler sh(dvdb, KernelKind::skip, scheds[1]);
+        const gpu::PackedSamples whole = sh.sample_rays(rays);
+        for (int world : {1, 3, 7}) {
+            long sm = 0;
+            std::int64_t covered = 0;
+            for (int rank = 0; rank < world; ++rank) {
+                const gpu::ShardRange sr = gpu::shard_range(std::int64_t(rays.size()), world, rank);
+                const gpu::PackedSamples part = sh.sample_shard(rays, world, rank);
+                sm += std::int64_t(part.size()) != sr.count;
+                for (std::int64_t r = 0; r < sr.count && sm == 0; ++r) {
+                    const std::size_t g = std::size_t(sr.first + r);
+                    sm += part.run(std::size_t(r)).samples != whole.run(g).samples;
+                    const auto off = part.packed_info[2 * r], cnt = part.packed_info[2 * r + 1];
+                    for (std::int64_t k = 0; k < cnt; ++k)
+                        sm += part.ray_indices[std::size_t(off + k)] != std::int32_t(g);
+                }
+                covered += sr.count;
+            }
+            EXPECT(sm == 0 && covered == std::int64_t(rays.size()), "world %d: shards differ from the batch",
+                   world);
+        }
+    }
     // single-ray drop-in
     const gpu::Sampler one(dvdb, KernelKind::skip, scheds[0]);
     EXPECT(one(rays[1234]).samples == run_sampler(rays[1234], sparse, KernelKind::skip, scheds[0]).samples,
