@@ -196,9 +196,16 @@ extern __shared__ int32_t sogk_dyn_smem[];
 #define SOGK_QUERY_CACHE 0 // 1: per-thread cached leaf (divergent miss path); 0: uniform walk
 #endif
 
+#ifndef SOGK_SMEM_TABLE
+#define SOGK_SMEM_TABLE 0 // 1: pass 1 stages a single-region VDB's child table in shared memory
+#endif
+
 // child table entry ci of `node` (the root entry of an in-grid region, >= 0)
 __device__ __forceinline__ int32_t table_at(const GridDev& g, int32_t node, int ci) {
-    return g.smem_tab ? sogk_dyn_smem[ci] : __ldg(g.table + (int64_t)node * 4096 + ci);
+#if SOGK_SMEM_TABLE
+    if (g.smem_tab) return sogk_dyn_smem[ci];
+#endif
+    return __ldg(g.table + (int64_t)node * 4096 + ci);
 }
 
 struct VdbCursor {

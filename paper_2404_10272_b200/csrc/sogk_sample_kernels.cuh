@@ -23,9 +23,6 @@ constexpr int kWriteBlock = 128;
 #ifndef SOGK_COUNT_MINB
 #define SOGK_COUNT_MINB 7 // pass-1 min resident blocks per SM: <= 72 registers (A/B: -2 % HDDA, -7 % DDA vs 76-88)
 #endif
-#ifndef SOGK_SMEM_TABLE
-#define SOGK_SMEM_TABLE 0 // 1: pass 1 stages a single-region VDB's child table in shared memory
-#endif
 
 // ---------------------------------------------------------------------------
 // warp / block scans
@@ -228,7 +225,7 @@ __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MIN
     count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
                  int32_t* __restrict__ counters, const SlabDev S) {
-    if (s.lv[0].smem_tab) { // stage the single-region child table (16 KB) in shared memory
+    if (SOGK_SMEM_TABLE && s.lv[0].smem_tab) { // stage the single-region child table (16 KB) in shared memory
         const int32_t node0 = __ldg(s.lv[0].root);
         const int4* tsrc = reinterpret_cast<const int4*>(s.lv[0].table + (int64_t)(node0 < 0 ? 0 : node0) * 4096);
         int4* tdst = reinterpret_cast<int4*>(sogk_dyn_smem);

@@ -7,4 +7,4 @@ python tools/ncu_summary.py /tmp/${TAG}.ncu-rep > gpurun_out/${TAG}_summary.txt 
 for K in count_kernel gather_kernel tail_kernel; do
   ncu -i /tmp/${TAG}.ncu-rep -k regex:$K --page source --csv --print-source sass > gpurun_out/${TAG}_${K}_sass.csv 2>/dev/null
 done
-cp /tmp/${TAG}.ncu-rep gpurun_out/ 2>/dev/null
+# (the .ncu-rep stays on the box: gpurun_out is capped at 64 MiB)
