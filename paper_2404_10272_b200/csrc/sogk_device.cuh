@@ -419,7 +419,10 @@ struct DdaAn { // DdaTraversal, traversal.hpp:120-193
 #endif
 // Kernels using the node analyzers or the cascade launch 1-D blocks of at most kGeomBlock
 // threads (per-thread shared-memory columns).
-constexpr int kGeomBlock = 128;
+#ifndef SOGK_BLOCK
+#define SOGK_BLOCK 128 // threads per block of the traversal kernels (pass 1, tail, cold write, traverse)
+#endif
+constexpr int kGeomBlock = SOGK_BLOCK;
 #if SOGK_HDDA_SMEM
 // The per-ray geometry lives in shared memory (one column per thread, SoA: conflict-free),
 // which keeps ~22 registers out of the traversal loop.

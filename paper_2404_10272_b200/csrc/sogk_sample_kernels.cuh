@@ -12,8 +12,8 @@
 
 namespace sogk {
 
-constexpr int kBlock = 128;
-constexpr int kWriteBlock = 128;
+constexpr int kBlock = kGeomBlock;
+constexpr int kWriteBlock = kGeomBlock;
 #ifndef SOGK_GATHER_SHORT
 #define SOGK_GATHER_SHORT 8
 #endif
