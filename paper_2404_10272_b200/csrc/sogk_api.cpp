@@ -263,6 +263,9 @@ struct RenderScratch {
     int64_t rb_n = 0;
     void* sb = nullptr;
     int64_t smp_cap = 0;
+    // smallest camera bound found not to fit a quarter of free memory: larger bounds skip the
+    // cudaMemGetInfo query (a driver call per frame whose latency varies run to run)
+    int64_t unfit_bound = INT64_MAX;
     int64_t* h_total = nullptr; // pinned
     static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
     int ensure_rays(int64_t n) {
@@ -303,6 +306,7 @@ struct RenderScratch {
         rb = sb = nullptr;
         h_total = nullptr;
         rb_n = smp_cap = 0;
+        unfit_bound = INT64_MAX;
     }
 };
 static std::map<std::pair<int, void*>, RenderScratch*>& render_registry() {
@@ -1596,13 +1600,15 @@ int sogk_render_camera(sogk_sampler* s, const sogk_scene* scene, const sogk_came
         const int64_t bound = per * n;
         if (bound <= rs->smp_cap) {
             fixed = true;
-        } else {
+        } else if (bound < rs->unfit_bound) {
             size_t fr = 0, tot = 0;
             if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) cudaGetLastError();
             if (double(bound) * RenderScratch::kSampleBytes <= 0.25 * double(fr)) {
                 st = rs->ensure_samples(bound, stream);
                 if (st) return st;
                 fixed = true;
+            } else {
+                rs->unfit_bound = bound;
             }
         }
     }
