@@ -12,7 +12,9 @@
  * Conventions
  *  - Limits: n < 2^32 rays per call; ray_indices are int32, so ray_index_base + n - 1 <=
  *    INT32_MAX when they are written; cells pack 10 bits per axis, so cells are refused
- *    for grids above 1024 voxels on an axis (SOGK_INVALID_ARG).
+ *    for grids above 1024 voxels on an axis (SOGK_INVALID_ARG); device rays and
+ *    packed_info / event_info must be 16-byte aligned (any cudaMalloc / torch allocation is),
+ *    events 8-byte (SOGK_INVALID_ARG otherwise); sample output arrays may have any alignment.
  *  - Every function returns an int status (sogk_status); no exceptions cross
  *    the boundary.  sogk_last_error() returns the thread-local message of the
  *    last failure.

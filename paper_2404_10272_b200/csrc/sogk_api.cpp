@@ -33,6 +33,12 @@ int fail(int status, const std::string& msg) {
     return status;
 }
 
+// Rays are read as 16-byte pairs and packed_info / event_info are {offset, count} pairs read and
+// written as one 16-byte access: a misaligned base would fault the kernel (a sticky context
+// error), so the entry points refuse it up front.
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+const char* const kAlign16 = "device rays and packed_info / event_info must be 16-byte aligned";
+
 int cuda_fail(cudaError_t e, const char* what) {
     if (e == cudaErrorMemoryAllocation)
         return fail(SOGK_OOM, std::string(what) + ": " + cudaGetErrorString(e));
@@ -1192,6 +1198,7 @@ static int count_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
     if (!d_stats) return fail(SOGK_INVALID_ARG, "stats buffer is NULL");
     if (n > 0 && (!d_packed || (!cam && !d_rays)))
         return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    if (n > 0 && (!aligned16(d_packed) || (!cam && !aligned16(d_rays)))) return fail(SOGK_INVALID_ARG, kAlign16);
     int st = s->wait_levels(stream);
     if (st) return st;
     CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
@@ -1283,6 +1290,7 @@ static int write_impl(sogk_sampler* s, const double* d_rays, const sogk_camera* 
                                       "cannot export cells");
     if (n == 0) return SOGK_OK;
     if (!d_packed || !ts || (!cam && !d_rays)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    if (!aligned16(d_packed) || (!cam && !aligned16(d_rays))) return fail(SOGK_INVALID_ARG, kAlign16);
     int st = s->wait_levels(stream);
     if (st) return st;
     CameraDev cd{};
@@ -1329,6 +1337,7 @@ int sogk_traverse_count(sogk_sampler* s, const double* d_rays, int64_t n, int64_
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
     if (!d_stats) return fail(SOGK_INVALID_ARG, "stats buffer is NULL");
     if (n > 0 && (!d_rays || !d_event_info)) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    if (n > 0 && (!aligned16(d_rays) || !aligned16(d_event_info))) return fail(SOGK_INVALID_ARG, kAlign16);
     int st = s->wait_levels(stream);
     if (st) return st;
     CK(cudaMemsetAsync(d_stats, 0, SOGK_STATS_LEN * sizeof(int64_t), S(stream)), "stats reset");
@@ -1356,6 +1365,8 @@ int sogk_traverse_write(sogk_sampler* s, const double* d_rays, int64_t n,
     if (n < 0) return fail(SOGK_INVALID_ARG, "negative ray count");
     if (n == 0) return SOGK_OK;
     if (!d_rays || !d_event_info || !d_events) return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    if (!aligned16(d_rays) || !aligned16(d_event_info) || (reinterpret_cast<uintptr_t>(d_events) & 7))
+        return fail(SOGK_INVALID_ARG, "device rays / event_info must be 16-byte aligned, events 8-byte");
     int st = s->wait_levels(stream);
     if (st) return st;
     CK(launch_traverse_write(s->v, s->dev, d_rays, n, d_event_info, d_events, S(stream)), "traverse launch");
@@ -1570,6 +1581,7 @@ int sogk_composite(const sogk_sampler* s, const sogk_scene* scene, const double*
     if (n == 0) return SOGK_OK;
     if (!d_rays || !d_packed_info || (!d_result && !d_rgb8))
         return fail(SOGK_INVALID_ARG, "NULL device buffer");
+    if (!aligned16(d_rays) || !aligned16(d_packed_info)) return fail(SOGK_INVALID_ARG, kAlign16);
     CK(launch_composite(s->v, s->dev, scene->dev, d_rays, n, d_packed_info, d_t_starts, d_result,
                         d_rgb8, S(stream)),
        "composite launch");
