@@ -68,8 +68,19 @@ extern "C" int sogk_grid_create_dense_broadcast(const sogk_transform* t, const u
     sogk_transform* d_t = nullptr;
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d_t), sizeof(sogk_transform));
     if (e != cudaSuccess) return sogk_last_error_set(SOGK_OOM, "broadcast scratch");
+    // the root validates its arguments before any collective; an invalid grid is broadcast as
+    // a zero transform so every rank fails the same way instead of waiting on the payload
     sogk_transform ht{};
-    if (is_root) ht = *t;
+    const char* root_err = nullptr;
+    if (is_root) {
+        const uint64_t v = uint64_t(t->res[0] > 0 ? t->res[0] : 0) * uint64_t(t->res[1] > 0 ? t->res[1] : 0) *
+                           uint64_t(t->res[2] > 0 ? t->res[2] : 0);
+        if (t->res[0] < 1 || t->res[1] < 1 || t->res[2] < 1 || !(t->voxel_size > 0.0))
+            root_err = "broadcast transform is invalid";
+        else if (nbytes != size_t((v + 7) / 8))
+            root_err = "payload size must be ceil(voxel_count / 8) bytes";
+        if (!root_err) ht = *t;
+    }
     if (is_root) e = cudaMemcpyAsync(d_t, &ht, sizeof ht, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
         r = N.bcast(d_t, d_t, sizeof(sogk_transform), kNcclUint8, root, nccl_comm, st);
@@ -84,10 +95,9 @@ extern "C" int sogk_grid_create_dense_broadcast(const sogk_transform* t, const u
     if (e != cudaSuccess) return sogk_last_error_set(SOGK_CUDA_ERROR, cudaGetErrorString(e));
     const uint64_t vox = uint64_t(ht.res[0]) * uint64_t(ht.res[1]) * uint64_t(ht.res[2]);
     const size_t need = size_t((vox + 7) / 8);
+    if (root_err) return sogk_last_error_set(SOGK_INVALID_ARG, root_err);
     if (ht.res[0] < 1 || ht.res[1] < 1 || ht.res[2] < 1 || !(ht.voxel_size > 0.0))
-        return sogk_last_error_set(SOGK_INVALID_ARG, "broadcast transform is invalid");
-    if (is_root && nbytes != need)
-        return sogk_last_error_set(SOGK_INVALID_ARG, "payload size must be ceil(voxel_count / 8) bytes");
+        return sogk_last_error_set(SOGK_INVALID_ARG, "broadcast transform is invalid (the root's arguments)");
     // 2) the payload, once, NCCL over NVLink
     uint8_t* d_bits = nullptr;
     e = cudaMalloc(reinterpret_cast<void**>(&d_bits), need);

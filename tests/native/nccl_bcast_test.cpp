@@ -58,6 +58,13 @@ int main() {
     // a NULL communicator is refused like the reference's invalid arguments
     sogk_grid* g = nullptr;
     bad += sogk_grid_create_dense_broadcast(&t, bits.data(), bits.size(), 0, nullptr, nullptr, &g) != SOGK_INVALID_ARG;
+    // a wrong payload size at the root is refused after a zero transform went out (every rank
+    // fails the same call instead of waiting on the payload broadcast); the communicator stays usable
+    bad += sogk_grid_create_dense_broadcast(&t, bits.data(), bits.size() - 1, 0, comms[0], nullptr, &g) !=
+           SOGK_INVALID_ARG;
+    sogk_grid* again = nullptr;
+    bad += sogk_grid_create_dense_broadcast(&t, bits.data(), bits.size(), 0, comms[0], nullptr, &again) != 0;
+    if (again) sogk_grid_destroy(again);
     std::printf("%s: broadcast grid == root payload (%zu bytes), SOG1 %zu bytes identical\n", bad ? "FAILED" : "OK",
                 bits.size(), n0);
     return bad ? 1 : 0;
