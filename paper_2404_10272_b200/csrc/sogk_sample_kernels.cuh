@@ -20,6 +20,9 @@ constexpr int kWriteBlock = kGeomBlock;
 #ifndef SOGK_CASC_MINB
 #define SOGK_CASC_MINB 5 // cascade variants: <= 96 registers (A/B cfg3: HDDA step -4 %, DDA -24 % vs 126)
 #endif
+#ifndef SOGK_REC_V4
+#define SOGK_REC_V4 1 // pass 1 writes each run record with one 128-bit store
+#endif
 #ifndef SOGK_COUNT_MINB
 #define SOGK_COUNT_MINB 7 // pass-1 min resident blocks per SM: <= 72 registers (A/B: -2 % HDDA, -7 % DDA vs 76-88)
 #endif
@@ -196,7 +199,16 @@ __device__ __forceinline__ void count_one(const SamplerDev& s, const Src& src, i
                     rec.first = first;
                     rec.cell = pack_cell(ev.ijk);
                     rec.sl = (uint32_t)filled | ((uint32_t)(ev.level | (ev.grid_level << 2)) << 24);
-                    row[nr++] = rec; // one 128-bit store per run
+#if SOGK_REC_V4
+                    { // one 128-bit store per run (the struct copy compiles to two 64-bit stores)
+                        const long long fb = __double_as_longlong(rec.first);
+                        *reinterpret_cast<int4*>(row + nr) =
+                            make_int4((int)(unsigned)fb, (int)(unsigned)(fb >> 32), (int)rec.cell, (int)rec.sl);
+                        ++nr;
+                    }
+#else
+                    row[nr++] = rec;
+#endif
                     filled += k;
                 } else { // the run that does not fit restarts in tail_kernel
                     ovf = true;
