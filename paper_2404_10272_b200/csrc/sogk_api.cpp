@@ -196,6 +196,7 @@ struct sogk_grid {
         g.prefix = prefix;
         g.leaves = leaves;
         g.table = table;
+        g.node0 = kNodeMulti;
         g.dist = dist;
         return g;
     }
@@ -1125,6 +1126,19 @@ int sogk_sampler_create(const sogk_grid* const* levels, int n_levels,
     for (int b = 0; b < n_levels; ++b) {
         s->dev.lv[b] = levels[b]->dev();
         s->lv[b] = levels[b];
+        // a single-region VDB (128^3 and below): its one root entry goes into the sampler's
+        // constant parameters, so the query's dependent chain is child table -> leaf word
+        const sogk_grid* L = levels[b];
+        if (SOGK_NODE0 && L->kind == SOGK_GRID_VDB && L->R[0] == 1 && L->R[1] == 1 && L->R[2] == 1 && L->root) {
+            int32_t r0 = 0;
+            cudaError_t e = L->wait_ready();
+            if (e == cudaSuccess) e = cudaMemcpy(&r0, L->root, sizeof r0, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) {
+                delete s;
+                return cuda_fail(e, "root entry");
+            }
+            s->dev.lv[b].node0 = r0;
+        }
         for (int a = 0; a < 3; ++a) s->max_res = std::max(s->max_res, levels[b]->t.res[a]);
     }
     s->dev.n_levels = n_levels;

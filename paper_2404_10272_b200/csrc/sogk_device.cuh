@@ -257,8 +257,13 @@ struct VdbCursor {
         // rays leave their leaves on different iterations, so most warp iterations ran the
         // ~45-instruction miss path for a handful of lanes (ncu: 3-10 of 32 active).
         const bool inb = in_bounds(g, ijk);
-        const int region = inb ? ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7) : 0;
-        const int32_t node = __ldg(g.root + region);
+        int32_t node;
+        if (SOGK_NODE0 && g.node0 != kNodeMulti) { // single region (uniform: a kernel parameter)
+            node = g.node0;
+        } else {
+            const int region = inb ? ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7) : 0;
+            node = __ldg(g.root + region);
+        }
         const int ci = ((((ijk[2] >> 3) & 15) * 16 + ((ijk[1] >> 3) & 15)) * 16) + ((ijk[0] >> 3) & 15);
         const int32_t code = table_at(g, node < 0 ? 0 : node, ci);
         const uint64_t w = __ldg(g.leaves + (int64_t)(code < 0 ? 0 : code) * 8 + (ijk[2] & 7));

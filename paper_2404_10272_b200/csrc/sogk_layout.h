@@ -28,6 +28,10 @@ constexpr int32_t kRootEmpty = -1;
 constexpr int32_t kRootOccupied = -2;
 constexpr int32_t kTileEmpty = -1;
 constexpr int32_t kTileOccupied = -2;
+#ifndef SOGK_NODE0
+#define SOGK_NODE0 1 // 1: a single-region VDB's root entry is a sampler constant (GridDev::node0)
+#endif
+constexpr int32_t kNodeMulti = -2147483647 - 1; // GridDev::node0: read the root per query
 constexpr int SOGK_CONSTANT_SCHED = 0;
 constexpr int SOGK_LINEAR_SCHED = 1;
 
@@ -46,6 +50,8 @@ struct GridDev {
     const uint32_t* prefix;
     const uint64_t* leaves;
     const int32_t* table;
+    int32_t node0;         // single-region VDB: its root entry, read once by the sampler (kNodeMulti:
+                           // several regions or not known, the query reads the root)
     const int32_t* dist;   // DistanceGrid (distance.hpp:15-43): chessboard distance per voxel
     int smem_tab;          // launch-local: the child table of this single-region VDB is staged
                            // in the kernel's dynamic shared memory (sogk_dyn_smem)
