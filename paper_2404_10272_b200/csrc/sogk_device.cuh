@@ -214,6 +214,9 @@ struct VdbCursor {
 
     __device__ __forceinline__ void reset() { lo[0] = lo[1] = lo[2] = kNoLeaf; leaf = 0; }
 
+    // ONE: 1 = single-region grid (the root entry is the kernel parameter g.node0), 0 = read the
+    // root, -1 = decide at run time from g.node0 (a warp-uniform branch)
+    template <int ONE = -1>
     __device__ __forceinline__ Query query(const GridDev& g, const int ijk[3]) {
         Query q;
 #if SOGK_QUERY_CACHE
@@ -258,7 +261,7 @@ struct VdbCursor {
         // ~45-instruction miss path for a handful of lanes (ncu: 3-10 of 32 active).
         const bool inb = in_bounds(g, ijk);
         int32_t node;
-        if (SOGK_NODE0 && g.node0 != kNodeMulti) { // single region (uniform: a kernel parameter)
+        if (ONE == 1 || (ONE < 0 && SOGK_NODE0 && g.node0 != kNodeMulti)) { // single region
             node = g.node0;
         } else {
             const int region = inb ? ((ijk[2] >> 7) * g.R[1] + (ijk[1] >> 7)) * g.R[0] + (ijk[0] >> 7) : 0;
@@ -446,7 +449,7 @@ __device__ __forceinline__ HddaGeomSmem& hdda_geom() {
 // cube of half-width d-1 around the voxel (d = chessboard distance, proven empty), with
 // low corner ijk - (d-1) instead of an extent-aligned VDB node; everything else -- exit
 // planes, argmin, clamp to t_exit, degenerate re-derivation, spin guard -- is identical.
-template <bool CD>
+template <bool CD, int ONE = -1> // ONE: VdbCursor::query's single-region mode
 struct NodeAn {
     static constexpr bool kHdda = !CD;
 #if SOGK_HDDA_SMEM
@@ -532,7 +535,7 @@ struct NodeAn {
             q.level = LV_VOXEL;
             q.occ = d == 0;
         } else {
-            q = cur.query(g, ijk);
+            q = cur.template query<ONE>(g, ijk);
         }
         ++lookups;
         // exit plane of the node on each axis (:218-228), mirrored: lo + ext walking up,

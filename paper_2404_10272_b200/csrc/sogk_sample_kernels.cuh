@@ -20,6 +20,9 @@ constexpr int kWriteBlock = kGeomBlock;
 #ifndef SOGK_CASC_MINB
 #define SOGK_CASC_MINB 5 // cascade variants: <= 96 registers (A/B cfg3: HDDA step -4 %, DDA -24 % vs 126)
 #endif
+#ifndef SOGK_ONE_TEMPLATE
+#define SOGK_ONE_TEMPLATE 1 // pass 1 compiled per HDDA query mode (single-region / root read), not branched
+#endif
 #ifndef SOGK_REC_V4
 #define SOGK_REC_V4 1 // pass 1 writes each run record with one 128-bit store
 #endif
@@ -165,7 +168,7 @@ __device__ __forceinline__ void count_invalid(long long r, int64_t* packed, uint
 // pass 1: per-ray counts, status, counters, slab samples, resume state
 // ---------------------------------------------------------------------------
 // one ray of pass 1 (the ray the j-th processing slot names: src.id(j))
-template <int AN, bool CASC, bool BR, int SCH, class Src>
+template <int AN, bool CASC, bool BR, int SCH, class Src, int ONE>
 __device__ __forceinline__ void count_one(const SamplerDev& s, const Src& src, int64_t j, int64_t* __restrict__ packed,
                                           uint8_t* __restrict__ status, int32_t* __restrict__ counters,
                                           const SlabDev& S, Stats5& acc) {
@@ -175,7 +178,7 @@ __device__ __forceinline__ void count_one(const SamplerDev& s, const Src& src, i
             count_invalid(r, packed, status, counters, acc);
             if (S.nruns) S.nruns[r] = 0;
         } else {
-            RunGen<BR, SCH, typename PickAn<AN, CASC>::type> gen;
+            RunGen<BR, SCH, typename PickAn<AN, CASC, ONE>::type> gen;
             gen.init(ray, s);
             RunRec* const row = S.runs + r * S.C;
             long long c = 0;
@@ -232,7 +235,8 @@ __device__ __forceinline__ void count_one(const SamplerDev& s, const Src& src, i
         }
 }
 
-template <int AN, bool CASC, bool BR, int SCH, class Src>
+// ONE (HDDA): 1 = every level is a single-region VDB (its root entry is GridDev::node0), 0 = not
+template <int AN, bool CASC, bool BR, int SCH, class Src, int ONE>
 __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MINB)
     count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MIN
     }
     Stats5 acc;
     const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (j < n) count_one<AN, CASC, BR, SCH, Src>(s, src, j, packed, status, counters, S, acc);
+    if (j < n) count_one<AN, CASC, BR, SCH, Src, ONE>(s, src, j, packed, status, counters, S, acc);
     acc.flush(stats); // warp-level: no block barrier, finished warps leave at once
 }
 
@@ -927,7 +931,16 @@ struct Launch {
             dyn = 4096 * sizeof(int32_t);
         }
         const unsigned grid = (unsigned)blocks;
-        count_kernel<AN, CASC, BR, SCH, Src>
+        if constexpr (AN == SOGK_HDDA && SOGK_ONE_TEMPLATE) { // single-region levels: no root read
+            bool one = SOGK_NODE0 != 0;
+            for (int b = 0; b < s.n_levels; ++b) one = one && s.lv[b].node0 != kNodeMulti;
+            if (one) {
+                count_kernel<AN, CASC, BR, SCH, Src, 1>
+                    <<<grid, kBlock, dyn, st>>>(s2, src, n, packed, stats, status, counters, S);
+                return cudaGetLastError();
+            }
+        }
+        count_kernel<AN, CASC, BR, SCH, Src, SOGK_ONE_TEMPLATE ? 0 : -1>
             <<<grid, kBlock, dyn, st>>>(s2, src, n, packed, stats, status, counters, S);
         return cudaGetLastError();
     }

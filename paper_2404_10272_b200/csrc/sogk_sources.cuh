@@ -61,10 +61,12 @@ struct RaysFromCamera {
     __device__ __forceinline__ Ray load(int64_t i) const { return pixel_ray(cam, first + i); }
 };
 
-template <int AN, bool CASC>
+// ONE: the HDDA query's single-region mode (VdbCursor::query): the count kernel is compiled for
+// single-region grids (1) and for the rest (0); other kernels decide at run time (-1)
+template <int AN, bool CASC, int ONE = -1>
 struct PickAn {
     using Sub = typename std::conditional<
-        AN == SOGK_HDDA, HddaAn, typename std::conditional<AN == SOGK_CD, CdAn, DdaAn>::type>::type;
+        AN == SOGK_HDDA, NodeAn<false, ONE>, typename std::conditional<AN == SOGK_CD, CdAn, DdaAn>::type>::type;
     using type = AnyAn<Sub, CASC>;
 };
 
