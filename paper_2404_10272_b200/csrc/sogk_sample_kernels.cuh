@@ -27,7 +27,10 @@ constexpr int kWriteBlock = kGeomBlock;
 #define SOGK_REC_V4 1 // pass 1 writes each run record with one 128-bit store
 #endif
 #ifndef SOGK_COUNT_MINB
-#define SOGK_COUNT_MINB 7 // pass-1 min resident blocks per SM: <= 72 registers (A/B: -2 % HDDA, -7 % DDA vs 76-88)
+#define SOGK_COUNT_MINB 7 // DDA pass-1 min resident blocks per SM: <= 72 registers (A/B: -7 % vs 76-88; 8: +4-10 %)
+#endif
+#ifndef SOGK_COUNT_MINB_NODE
+#define SOGK_COUNT_MINB_NODE 8 // HDDA / CD pass 1: <= 64 registers, 24 B stack (A/B vs 7: HDDA cfg2 -1.7 %, cfg4 -2.5 %)
 #endif
 
 // ---------------------------------------------------------------------------
@@ -237,7 +240,8 @@ __device__ __forceinline__ void count_one(const SamplerDev& s, const Src& src, i
 
 // ONE (HDDA): 1 = every level is a single-region VDB (its root entry is GridDev::node0), 0 = not
 template <int AN, bool CASC, bool BR, int SCH, class Src, int ONE>
-__global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB : SOGK_COUNT_MINB)
+__global__ void __launch_bounds__(kBlock, CASC ? SOGK_CASC_MINB
+                                               : (AN == SOGK_DDA ? SOGK_COUNT_MINB : SOGK_COUNT_MINB_NODE))
     count_kernel(const __grid_constant__ SamplerDev s, const Src src, int64_t n, int64_t* __restrict__ packed,
                  int64_t* __restrict__ stats, uint8_t* __restrict__ status,
                  int32_t* __restrict__ counters, const SlabDev S) {
